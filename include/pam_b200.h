@@ -1,0 +1,226 @@
+/*
+ * pam_b200.h — C-ABI of the B200-native PAM hot path (libpam_b200.so).
+ *
+ * Every entry point is `extern "C"`, takes plain pointers and sizes (no torch
+ * or C++ types), and returns an int status (PAM_OK on success).  Reals are
+ * IEEE binary64 throughout; indices are int64 unless stated.
+ *
+ * Two layers:
+ *
+ *   1. Device-pointer, stream-ordered batch entry points (`pam_*_f64`).  All
+ *      array arguments are DEVICE pointers; the call enqueues kernels on
+ *      `stream` (a cudaStream_t passed as void*, NULL = legacy default stream)
+ *      and returns without synchronising.  Data-dependent errors (non-positive
+ *      field value, point outside all boxes, degenerate Shepard denominator)
+ *      are reported through a caller-owned DEVICE int64[2] "error word"
+ *      `err` = {code, first offending index}; initialise it with
+ *      pam_err_reset() and read it after the stream is synchronised.
+ *
+ *   2. Host-pointer, synchronous seams (`pam_*_host_f64`) whose arguments
+ *      mirror the reference function they replace one-for-one, so the
+ *      reference package can bind them with ctypes.
+ *
+ * Ragged batches ("subdomains", reference partition.py:45-93) are described
+ * by CSR-style offsets:
+ *   row_off[S+1]  : cells (sample rows) of subdomain s are rows
+ *                   [row_off[s], row_off[s+1]) of the packed point/value
+ *                   arrays, ascending global cell index (fields.py:61-73).
+ *   dict_off[S]   : first dictionary slot of subdomain s in the packed
+ *                   centre/width/beta arrays; dict_cap[S] slots reserved.
+ *   m_cur[S]      : current dictionary size M_s (int32, <= dict_cap[s]).
+ *   w_off[S]      : offset (in doubles) of subdomain s's design matrix in
+ *                   the packed W buffer; column-major with leading dimension
+ *                   ld[s] (int32, multiple of 16): W_s[i, j] = W[w_off+j*ld+i].
+ *
+ * Citations are relative to the reference package root pkg/src/fieldfit/.
+ */
+#ifndef PAM_B200_H
+#define PAM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes --------------------------------------------------------- */
+#define PAM_OK 0
+#define PAM_ERR_CUDA 1         /* CUDA runtime error (launch/alloc/copy)           */
+#define PAM_ERR_ARG 2          /* invalid argument (sizes, dims, null pointers)    */
+#define PAM_ERR_OUTSIDE 3      /* point outside all boxes  (geometry.py:255-257)   */
+#define PAM_ERR_DEGENERATE 4   /* Shepard denominator degenerate (rbf.py:165-166)  */
+#define PAM_ERR_NONPOSITIVE 5  /* field value not positive (elastic_net.py:200-204) */
+#define PAM_ERR_UNSUPPORTED 6  /* shape outside the compiled kernel envelope       */
+#define PAM_ERR_NONFINITE 7    /* non-finite design/target (elastic_net.py:81-82)  */
+
+/* Version / capability probe: returns PAM_ABI_VERSION. */
+#define PAM_ABI_VERSION 1
+int pam_abi_version(void);
+/* Last CUDA error string recorded by the library (host memory, static). */
+const char* pam_last_error(void);
+/* Largest subdomain sample count the CD kernel accepts (rows per subdomain). */
+int64_t pam_cd_max_rows(void);
+
+/* err[0] = 0 (no error), err[1] = INT64_MAX. Device pointer. */
+int pam_err_reset(int64_t* err, void* stream);
+
+/* ---- K0: log transform + positivity (elastic_net.py:197-205) ------------- */
+/* y[i] = log(values[i]); first i with !(values[i] > 0) -> err {NONPOSITIVE, i}. */
+int pam_log_values_f64(const double* values, int64_t n, double* y, int64_t* err,
+                       void* stream);
+
+/* ---- K1: Shepard design-matrix assembly ----------------------------------
+ * Replaces RbfDictionary.log_features + assemble_features + shepard_normalize
+ * = shepard_features (rbf.py:79-91, 123-149).  For every active subdomain s
+ * and every row i < N_s, column j < m_cur[s]:
+ *   L[i,j] = -(sum_k (x_ik - c_jk)^2) * (1 / (2 w_j^2))   (einsum order, F9)
+ *   W[i,j] = exp(L[i,j] - max_j L[i,:]) / sum_j exp(L[i,j] - max_j L[i,:])
+ * written column-major into W (see w_off/ld).  `active` may be NULL.
+ * mode 0 = Shepard weights W (above); mode 1 = raw exponents L
+ * (log_features); mode 2 = raw exp(L) (assemble_features values). */
+int pam_assemble_f64(int dim, int64_t S, const int64_t* row_off, const double* pts,
+                     const int64_t* dict_off, const int32_t* m_cur,
+                     const double* centres, const double* widths,
+                     const int64_t* w_off, const int32_t* ld, const int32_t* active,
+                     int32_t max_rows, int mode, double* W, void* stream);
+
+/* Row normalisation of a row-major (N, M) feature matrix (shepard_normalize,
+ * rbf.py:131-144).  mode 1: input holds exponents L -> exp(L - rowmax) /
+ * rowsum.  mode 0: input holds raw values -> v / rowsum; a row whose sum is
+ * <= 0 reports err {DEGENERATE, row} ("row j ... sums to zero"). */
+int pam_row_normalize_f64(int64_t N, int64_t M, const double* in, int mode, double* out,
+                          int64_t* err, void* stream);
+
+/* Subdomain batch gather from a structured mesh + make_partition grid
+ * (FieldData.subdomain over Partition.boxes, fields.py:61-73,
+ * partition.py:41-42, 73-92).  Cells of subdomain s = (sz*py+sy)*px+sx in
+ * ascending global index (x fastest) land in rows [row_off[s], row_off[s+1]);
+ * centroids are recomputed as lo_k + (i_k + 0.5) * d_k (geometry.py:122-132,
+ * bit-identical), values gathered, global cell ids written to cell_idx. */
+int pam_gather_cells_f64(int dim, const int64_t* counts, const int32_t* shape,
+                         const double* lo, const double* d, const double* values,
+                         int64_t S, const int64_t* row_off, double* pts_out,
+                         double* vals_out, int64_t* cell_idx_out, void* stream);
+
+/* ---- K2b: batched cyclic coordinate descent -------------------------------
+ * Replaces fit() + _cd_sweeps_jit (elastic_net.py:66-161) for every active
+ * subdomain at once, one warp per subdomain fit, design-matrix columns
+ * streamed HBM->SMEM with cp.async.bulk (TMA) + mbarrier.  Residual form:
+ *   col_sq = sum_i W_ij^2, denom = col_sq + lam2, r = y - W beta0,
+ *   sweeps in fixed order j = 0..M-1, soft threshold, stop when
+ *   max|delta| <= tol * max(1, max|beta|) or max_iters sweeps have run.
+ * beta (packed like centres, dict_off) is the warm start on entry and the
+ * solution on exit.  Outputs per subdomain: sweeps, converged, objective
+ * (= history[sweeps-1]).  hist/hist_off may be NULL; otherwise the per-sweep
+ * objective of subdomain s is written to hist[hist_off[s] + sweep]. */
+int pam_cd_f64(int64_t S, const int64_t* order, const int64_t* row_off, const double* y,
+               const int64_t* dict_off, const int32_t* m_cur, const int64_t* w_off,
+               const int32_t* ld, const double* W, const double* lam1, const double* lam2,
+               const double* tol, const int32_t* max_iters, const int32_t* active,
+               int32_t max_rows, double* beta, double* col_sq, int32_t* sweeps,
+               int32_t* converged, double* objective, double* hist, const int64_t* hist_off,
+               void* stream);
+/* `order` (nullable): processing order of the S subdomains (longest first
+ * balances the ragged batch); results do not depend on it.
+ * pam_cd_ex_f64 adds `flags`: 1 = col_sq given (not recomputed), 2 = y holds
+ * the initial residual r (no warm-start pass), 4 = write the final residual
+ * back into y.  The host seam below uses 1|2|4. */
+int pam_cd_ex_f64(int64_t S, const int64_t* order, const int64_t* row_off, double* y,
+                  const int64_t* dict_off, const int32_t* m_cur, const int64_t* w_off,
+                  const int32_t* ld, const double* W, const double* lam1, const double* lam2,
+                  const double* tol, const int32_t* max_iters, const int32_t* active,
+                  int32_t max_rows, double* beta, double* col_sq, int32_t* sweeps,
+                  int32_t* converged, double* objective, double* hist, const int64_t* hist_off,
+                  int flags, void* stream);
+
+/* ---- K3: residual indicators + L2 misfit parts -----------------------------
+ * Replaces residual_indicators (adaptive.py:133-138) with cell_quadrature
+ * (geometry.py:204-224) and l2_misfit_parts (fields.py:113-121).  For each
+ * active subdomain: R[i] = sum_l w_l (K*(x_i + off_l) - K_i)^2 with
+ * K* = exp(shepard_eval) when log_flag, and parts[2s] = num, parts[2s+1] =
+ * sum(w) * sum(K_i^2), rmax[s] = max_i R[i].  quad_order in {1, 2}. */
+int pam_residual_f64(int dim, int64_t S, const int64_t* row_off, const double* pts,
+                     const double* values, const int64_t* dict_off,
+                     const int32_t* m_cur, const double* centres,
+                     const double* widths, const double* beta,
+                     const int32_t* quad_order, const double* qoff, const double* qw,
+                     int32_t log_flag, const int32_t* active, int32_t max_rows,
+                     double* R, double* parts, double* rmax, int64_t* err, void* stream);
+/* qoff: ((1 + 2^dim), dim) quadrature offsets from the centroid, row 0 the
+ * order-1 point (zeros), rows 1.. the order-2 tensor Gauss points in the
+ * reference's meshgrid('ij') order; qw: matching weights (cell measure / n_q).
+ * Both are built on the host with the reference's own expressions. */
+
+/* ---- K3b: stable top-K marking (adaptive.py:141-152) ----------------------
+ * marked[s*kcap + t] = t-th cell (local row index) of subdomain s in
+ * lexsort((idx, -R)) order restricted to R > 0, t < k_top[s]; n_marked[s]. */
+int pam_mark_f64(int64_t S, const int64_t* row_off, const double* R,
+                 const int32_t* k_top, const int32_t* active, int32_t kcap,
+                 int32_t* marked, int32_t* n_marked, void* stream);
+
+/* ---- K3c: enrichment (adaptive.py:155-210) --------------------------------
+ * For marked cell t of subdomain s: parent = lexsort((idx, width, d2))[0]
+ * with d2 = np.sum order, width = eta * w_parent, candidates
+ * clamp(x_T + off_q * cell_size) dropped when an EXISTING entry matches to
+ * <= 1e-12 on every coordinate and the width.  Survivors are appended in
+ * (marked, offset) order at slot m_cur[s] onwards with generation `gen`;
+ * beta of new slots is zeroed; m_cur[s] and n_added[s] are updated.
+ * offsets: (S, mq_cap, dim) packed, m_q[s] used per subdomain.  A
+ * subdomain whose survivors would overflow dict_cap reports
+ * err {UNSUPPORTED, s} and adds nothing.
+ * box_lo/box_hi: (S, dim). */
+int pam_enrich_f64(int dim, int64_t S, const int64_t* row_off, const double* pts,
+                   const int32_t* marked, const int32_t* n_marked, int32_t kcap,
+                   const double* eta, const int32_t* m_q, int32_t mq_cap,
+                   const double* offsets, const double* cell_size,
+                   const double* box_lo, const double* box_hi,
+                   const int64_t* dict_off, const int32_t* dict_cap, int32_t* m_cur,
+                   double* centres, double* widths, int32_t* gens, double* beta,
+                   int32_t gen, const int32_t* active, int32_t* n_added,
+                   int64_t* err, void* stream);
+
+/* ---- K4: global evaluation ------------------------------------------------
+ * Replaces GlobalSurrogate.evaluate (partition.py:132-143) = locate_many
+ * (geometry.py:242-258) + LocalSurrogate.evaluate (rbf.py:152-192).
+ * Boxes form a tensor grid: edges_k (shape[k]+1 values per axis, host-
+ * identical to partition.py:59), open upper faces except the last box per
+ * axis.  owner = (sz*py + sy)*px + sx.  Points outside -> err {OUTSIDE, j}.
+ * out[j] = exp(v_j) (log_flag) or v_j, in input order.  `work` is scratch of
+ * pam_eval_workspace_bytes(P, S) bytes. */
+int64_t pam_eval_workspace_bytes(int64_t P, int64_t S);
+int pam_locate_f64(int dim, int64_t P, const double* pts, const int32_t* shape,
+                   const double* edges, int64_t* owner, int64_t* err, void* stream);
+int pam_eval_f64(int dim, int64_t P, const double* pts, const int32_t* shape,
+                 const double* edges, int64_t S, const int64_t* dict_off,
+                 const int32_t* m_cur, const double* centres, const double* widths,
+                 const double* beta, const int32_t* log_flag, double* out,
+                 void* work, int64_t* err, void* stream);
+
+/* Shepard evaluation of ONE dictionary at P points (rbf.py:152-167):
+ * out[j] = (sum_m e_jm beta_m) / (sum_m e_jm), e = exp(L - rowmax). */
+int pam_shepard_eval_f64(int dim, int64_t P, const double* pts, int64_t M,
+                         const double* centres, const double* widths,
+                         const double* beta, int32_t exp_out, double* out,
+                         int64_t* err, void* stream);
+
+/* ---- host-pointer synchronous seams (drop-in for the reference) ---------- */
+
+/* Exact signature of _cd_sweeps_jit (elastic_net.py:113): W is the (n, m)
+ * Fortran-ordered design matrix, beta/r/history are updated in place.
+ * Returns status; *sweeps, *converged receive the loop's return tuple. */
+int pam_cd_sweeps_host_f64(const double* W_fortran, int64_t n, int64_t m,
+                           const double* col_sq, const double* denom, double lam1,
+                           double lam2, double tol, int64_t max_iters, double* beta,
+                           double* r, double* history, int64_t* sweeps,
+                           int32_t* converged);
+
+/* shepard_eval(points, dictionary, beta) (rbf.py:152-167) on host arrays;
+ * *err_index receives the first offending point on PAM_ERR_DEGENERATE. */
+int pam_shepard_eval_host_f64(int dim, int64_t P, const double* pts, int64_t M,
+                              const double* centres, const double* widths,
+                              const double* beta, double* out, int64_t* err_index);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PAM_B200_H */

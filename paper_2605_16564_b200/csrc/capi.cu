@@ -1,0 +1,141 @@
+// capi.cu — library plumbing (status strings) and the host-pointer,
+// synchronous seams that let the CPU reference bind the device kernels
+// one-for-one:
+//
+//   pam_cd_sweeps_host_f64     <-> _cd_sweeps_jit       (elastic_net.py:113-161)
+//   pam_shepard_eval_host_f64  <-> shepard_eval         (rbf.py:152-167)
+#include "pam_common.cuh"
+
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+extern "C" int pam_cd_ex_f64(int64_t S, const int64_t* order, const int64_t* row_off, double* y,
+                             const int64_t* dict_off, const int32_t* m_cur, const int64_t* w_off,
+                             const int32_t* ld, const double* W, const double* lam1,
+                             const double* lam2, const double* tol, const int32_t* max_iters,
+                             const int32_t* active, int32_t max_rows, double* beta, double* col_sq,
+                             int32_t* sweeps, int32_t* converged, double* objective, double* hist,
+                             const int64_t* hist_off, int flags, void* stream);
+
+namespace pam {
+
+static char g_last_error[512] = "";
+
+void set_last_error(const char* msg) {
+  strncpy(g_last_error, msg, sizeof(g_last_error) - 1);
+  g_last_error[sizeof(g_last_error) - 1] = '\0';
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+  snprintf(g_last_error, sizeof(g_last_error), "%s: %s (%s)", where, cudaGetErrorName(e),
+           cudaGetErrorString(e));
+  return PAM_ERR_CUDA;
+}
+
+// RAII device buffer for the host seams
+struct DevBuf {
+  void* p = nullptr;
+  cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, std::max<size_t>(bytes, 16)); }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+}  // namespace pam
+
+using namespace pam;
+
+extern "C" int pam_abi_version(void) { return PAM_ABI_VERSION; }
+extern "C" const char* pam_last_error(void) { return g_last_error; }
+
+extern "C" int pam_cd_sweeps_host_f64(const double* W_fortran, int64_t n, int64_t m,
+                                      const double* col_sq, const double* denom, double lam1,
+                                      double lam2, double tol, int64_t max_iters, double* beta,
+                                      double* r, double* history, int64_t* sweeps_out,
+                                      int32_t* converged_out) {
+  (void)denom;  // denom == col_sq + lam2 by construction (elastic_net.py:86); recomputed on device
+  if (n < 1 || m < 1 || max_iters < 1 || max_iters > 0x7fffffff || !W_fortran || !col_sq || !beta ||
+      !r)
+    return PAM_ERR_ARG;
+  if (n > pam_cd_max_rows()) return PAM_ERR_UNSUPPORTED;
+  const int64_t ld = (n + 15) / 16 * 16;
+  DevBuf dW, dcs, db, dr, dmeta, dres, dh;
+  PAM_CUDA_CHECK(dW.alloc(sizeof(double) * ld * m));
+  PAM_CUDA_CHECK(dcs.alloc(sizeof(double) * m));
+  PAM_CUDA_CHECK(db.alloc(sizeof(double) * m));
+  PAM_CUDA_CHECK(dr.alloc(sizeof(double) * n));
+  PAM_CUDA_CHECK(dh.alloc(sizeof(double) * max_iters));
+  // meta: row_off[2], dict_off[1], w_off[1], hist_off[1] (int64); m_cur, ld, max_iters (int32)
+  PAM_CUDA_CHECK(dmeta.alloc(256));
+  PAM_CUDA_CHECK(dres.alloc(256));
+  PAM_CUDA_CHECK(cudaMemcpy2D(dW.p, ld * sizeof(double), W_fortran, n * sizeof(double),
+                              n * sizeof(double), m, cudaMemcpyHostToDevice));
+  PAM_CUDA_CHECK(cudaMemcpy(dcs.p, col_sq, sizeof(double) * m, cudaMemcpyHostToDevice));
+  PAM_CUDA_CHECK(cudaMemcpy(db.p, beta, sizeof(double) * m, cudaMemcpyHostToDevice));
+  PAM_CUDA_CHECK(cudaMemcpy(dr.p, r, sizeof(double) * n, cudaMemcpyHostToDevice));
+  struct Meta {
+    int64_t row_off[2], dict_off, w_off, hist_off;
+    double lam1, lam2, tol;
+    int32_t m_cur, ld, max_iters, pad;
+  } meta{{0, n}, 0, 0, 0, lam1, lam2, tol, (int32_t)m, (int32_t)ld, (int32_t)max_iters, 0};
+  PAM_CUDA_CHECK(cudaMemcpy(dmeta.p, &meta, sizeof(meta), cudaMemcpyHostToDevice));
+  Meta* dm = dmeta.as<Meta>();
+  int32_t* res_i = dres.as<int32_t>();  // sweeps, converged
+  double* res_d = reinterpret_cast<double*>(res_i + 4);
+  int rc = pam_cd_ex_f64(1, nullptr, dm->row_off, dr.as<double>(), &dm->dict_off, &dm->m_cur,
+                         &dm->w_off, &dm->ld, dW.as<double>(), &dm->lam1, &dm->lam2, &dm->tol,
+                         &dm->max_iters, nullptr, (int32_t)n, db.as<double>(), dcs.as<double>(),
+                         res_i, res_i + 1, res_d, dh.as<double>(), &dm->hist_off,
+                         /*COLSQ_GIVEN|R_GIVEN|WRITE_R*/ 1 | 2 | 4, nullptr);
+  if (rc != PAM_OK) return rc;
+  PAM_CUDA_CHECK(cudaDeviceSynchronize());
+  int32_t ri[2];
+  PAM_CUDA_CHECK(cudaMemcpy(ri, res_i, sizeof(ri), cudaMemcpyDeviceToHost));
+  PAM_CUDA_CHECK(cudaMemcpy(beta, db.p, sizeof(double) * m, cudaMemcpyDeviceToHost));
+  PAM_CUDA_CHECK(cudaMemcpy(r, dr.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  if (history)
+    PAM_CUDA_CHECK(cudaMemcpy(history, dh.p, sizeof(double) * ri[0], cudaMemcpyDeviceToHost));
+  if (sweeps_out) *sweeps_out = ri[0];
+  if (converged_out) *converged_out = ri[1];
+  return PAM_OK;
+}
+
+extern "C" int pam_shepard_eval_host_f64(int dim, int64_t P, const double* pts, int64_t M,
+                                         const double* centres, const double* widths,
+                                         const double* beta, double* out, int64_t* err_index) {
+  if (dim < 1 || dim > 3 || P < 0 || M < 1 || !pts || !centres || !widths || !beta || !out)
+    return PAM_ERR_ARG;
+  if (P == 0) return PAM_OK;
+  DevBuf dp, dc, dw, db, dout, derr;
+  PAM_CUDA_CHECK(dp.alloc(sizeof(double) * P * dim));
+  PAM_CUDA_CHECK(dc.alloc(sizeof(double) * M * dim));
+  PAM_CUDA_CHECK(dw.alloc(sizeof(double) * M));
+  PAM_CUDA_CHECK(db.alloc(sizeof(double) * M));
+  PAM_CUDA_CHECK(dout.alloc(sizeof(double) * P));
+  PAM_CUDA_CHECK(derr.alloc(sizeof(int64_t) * 2));
+  PAM_CUDA_CHECK(cudaMemcpy(dp.p, pts, sizeof(double) * P * dim, cudaMemcpyHostToDevice));
+  PAM_CUDA_CHECK(cudaMemcpy(dc.p, centres, sizeof(double) * M * dim, cudaMemcpyHostToDevice));
+  PAM_CUDA_CHECK(cudaMemcpy(dw.p, widths, sizeof(double) * M, cudaMemcpyHostToDevice));
+  PAM_CUDA_CHECK(cudaMemcpy(db.p, beta, sizeof(double) * M, cudaMemcpyHostToDevice));
+  int rc = pam_err_reset(derr.as<int64_t>(), nullptr);
+  if (rc != PAM_OK) return rc;
+  rc = pam_shepard_eval_f64(dim, P, dp.as<double>(), M, dc.as<double>(), dw.as<double>(),
+                            db.as<double>(), 0, dout.as<double>(), derr.as<int64_t>(), nullptr);
+  if (rc != PAM_OK) return rc;
+  PAM_CUDA_CHECK(cudaDeviceSynchronize());
+  int64_t e[2];
+  PAM_CUDA_CHECK(cudaMemcpy(e, derr.p, sizeof(e), cudaMemcpyDeviceToHost));
+  PAM_CUDA_CHECK(cudaMemcpy(out, dout.p, sizeof(double) * P, cudaMemcpyDeviceToHost));
+  if (e[0] != 0) {
+    if (err_index) *err_index = e[1];
+    return (int)e[0];
+  }
+  return PAM_OK;
+}

@@ -1,0 +1,602 @@
+"""Half-open decomposition, batched GPU fitting and global surrogates.
+
+Mirror of reference partition.py:1-217 (+ the text persistence 220-347).
+
+* ``make_partition(mesh, px, py=1, pz=1)`` — the reference's edges
+  ``lo + (hi-lo)*arange(p+1)/p`` and integer cell map, extended to 3D.
+* ``fit_parallel`` keeps its signature; instead of one process-pool task per
+  subdomain it builds the ragged batch on the device (``pam_gather_cells_f64``)
+  and runs every subdomain's adaptive loop at once in the FitEngine.
+  ``workers`` is accepted and ignored: results never depend on it
+  (partition.py:175-179).
+* ``GlobalSurrogate.evaluate`` is one fused device pass (``pam_eval_f64``:
+  locate + owner sort + Shepard sum + exp), order preserving.
+"""
+
+from __future__ import annotations
+
+import io
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .adaptive import AdaptiveConfig, RoundReport
+from .errors import DataError
+from .fields import FieldData, SubdomainField
+from .geometry import Box, Mesh, build_mesh, grid_edges
+from .rbf import LocalSurrogate, RbfDictionary, centroid_dictionary, lattice_dictionary
+
+SURROGATE_FORMAT = "fieldfit-surrogate"
+SURROGATE_VERSION = 1
+
+
+@dataclass(frozen=True)
+class Partition:
+    """Decomposition of a mesh into a (px[, py[, pz]]) grid of half-open boxes."""
+
+    mesh: Mesh
+    shape: tuple[int, ...]
+    boxes: tuple[Box, ...]
+    cell_to_subdomain: np.ndarray
+
+    @property
+    def n_subdomains(self) -> int:
+        return len(self.boxes)
+
+    def subdomain_fields(self, data: FieldData) -> list[SubdomainField]:
+        return [data.subdomain(b) for b in self.boxes]
+
+    @property
+    def grid(self):
+        """(shape, per-axis edges) when the boxes form a tensor grid, else None."""
+        g = self.__dict__.get("_grid", False)
+        if g is False:
+            g = grid_edges(self.boxes)
+            object.__setattr__(self, "_grid", g)
+        return g
+
+    def is_cell_aligned(self) -> bool:
+        """True for make_partition grids: boxes are unions of whole cells."""
+        g = self.grid
+        if g is None or tuple(g[0]) != tuple(self.shape) or len(self.shape) != self.mesh.dim:
+            return False
+        if any(n % p for n, p in zip(self.mesh.counts, self.shape)):
+            return False
+        for k, (n, p) in enumerate(zip(self.mesh.counts, self.shape)):
+            lo, hi = self.mesh.bounds[k]
+            if not np.array_equal(g[1][k], lo + (hi - lo) * np.arange(p + 1) / p):
+                return False
+        return True
+
+
+def make_partition(mesh: Mesh, px: int, py: int = 1, pz: int = 1) -> Partition:
+    """Split a mesh into px (x py (x pz)) equal boxes of whole cells (partition.py:45-93)."""
+    shape = (px, py, pz)[: mesh.dim]
+    if mesh.dim == 1 and py != 1:
+        raise ValueError("py must be 1 for a 1-D mesh")
+    if mesh.dim <= 2 and pz != 1:
+        raise ValueError(f"pz must be 1 for a {mesh.dim}-D mesh")
+    for n, p, axis in zip(mesh.counts, shape, "xyz"):
+        if p < 1:
+            raise ValueError(f"p{axis} must be >= 1, got {p}")
+        if n % p != 0:
+            raise ValueError(f"p{axis}={p} does not divide n{axis}={n}")
+
+    per_axis = []
+    for k, (n, p) in enumerate(zip(mesh.counts, shape)):
+        lo, hi = mesh.bounds[k]
+        per_axis.append(lo + (hi - lo) * np.arange(p + 1) / p)
+
+    boxes = []
+    for multi in np.ndindex(*shape[::-1]):
+        m = multi[::-1]  # x fastest, then y, then z (partition.py:73-81)
+        boxes.append(
+            Box(
+                lo=tuple(float(per_axis[k][m[k]]) for k in range(mesh.dim)),
+                hi=tuple(float(per_axis[k][m[k] + 1]) for k in range(mesh.dim)),
+                open_hi=tuple(m[k] < shape[k] - 1 for k in range(mesh.dim)),
+            )
+        )
+
+    # integer index arithmetic keeps every cell in exactly one subdomain (83-92)
+    cells_per = [n // p for n, p in zip(mesh.counts, shape)]
+    nx = mesh.counts[0]
+    cell_idx = np.arange(mesh.n_cells)
+    owner = (cell_idx % nx) // cells_per[0]
+    if mesh.dim >= 2:
+        ny = mesh.counts[1]
+        sy = ((cell_idx // nx) % ny) // cells_per[1]
+        owner = sy * shape[0] + owner
+    if mesh.dim == 3:
+        sz = (cell_idx // (nx * mesh.counts[1])) // cells_per[2]
+        owner = sz * (shape[0] * shape[1]) + owner
+    return Partition(mesh=mesh, shape=shape, boxes=tuple(boxes), cell_to_subdomain=owner)
+
+
+@dataclass(frozen=True)
+class DictionarySpec:
+    """Initial dictionary layout: one centre per cell, or a g-lattice (partition.py:96-112)."""
+
+    sigma: float
+    lattice: int | None = None
+
+    def __post_init__(self):
+        if self.sigma <= 0:
+            raise ValueError(f"sigma must be positive, got {self.sigma}")
+        if self.lattice is not None and self.lattice < 1:
+            raise ValueError(f"lattice resolution must be >= 1, got {self.lattice}")
+
+    def build(self, sub: SubdomainField) -> RbfDictionary:
+        if self.lattice is None:
+            return centroid_dictionary(sub.centroids, self.sigma)
+        return lattice_dictionary(sub.box, self.lattice, self.sigma)
+
+
+class DeviceSurrogate:
+    """Packed dictionaries of all subdomains resident in HBM (K4 operand)."""
+
+    def __init__(self, dim, dict_off, m_cur, centres, widths, beta, log_flag):
+        self.dim = dim
+        self.d_dict_off = dict_off
+        self.d_m_cur = m_cur
+        self.d_centres = centres
+        self.d_widths = widths
+        self.d_beta = beta
+        self.d_log = log_flag
+
+    @classmethod
+    def from_locals(cls, locals_):
+        from . import _native as nat
+
+        dim = locals_[0].dictionary.dim
+        m = np.array([len(l.dictionary) for l in locals_], dtype=np.int64)
+        off = np.concatenate([[0], np.cumsum(m)[:-1]]).astype(np.int64)
+        return cls(
+            dim,
+            nat.to_dev(off),
+            nat.to_dev(m.astype(np.int32)),
+            nat.to_dev(np.concatenate([l.dictionary.centers for l in locals_]).reshape(-1)),
+            nat.to_dev(np.concatenate([l.dictionary.widths for l in locals_])),
+            nat.to_dev(np.concatenate([l.beta for l in locals_])),
+            nat.to_dev(np.array([int(l.log_transform) for l in locals_], dtype=np.int32)),
+        )
+
+
+@dataclass(frozen=True)
+class GlobalSurrogate:
+    """Per-subdomain surrogates assembled over a partition (partition.py:115-143)."""
+
+    partition: Partition
+    locals: tuple[LocalSurrogate, ...]
+    metadata: dict = field(default_factory=dict)
+
+    def __post_init__(self):
+        if len(self.locals) != self.partition.n_subdomains:
+            raise ValueError("one local surrogate required per subdomain")
+
+    # -- device cache ---------------------------------------------------
+    def _device(self) -> DeviceSurrogate:
+        ds = self.__dict__.get("_device_cache")
+        if ds is None:
+            ds = DeviceSurrogate.from_locals(self.locals)
+            object.__setattr__(self, "_device_cache", ds)
+        return ds
+
+    def attach_device(self, ds: DeviceSurrogate):
+        object.__setattr__(self, "_device_cache", ds)
+
+    def _grid_dev(self):
+        from . import _native as nat
+
+        g = self.__dict__.get("_grid_cache")
+        if g is None:
+            grid = self.partition.grid
+            if grid is None:
+                raise ValueError(
+                    "partition boxes do not form a half-open tensor grid; GlobalSurrogate.evaluate "
+                    "requires a make_partition-style decomposition"
+                )
+            shape, edges = grid
+            g = (len(shape), nat.to_dev(np.asarray(shape, dtype=np.int32)),
+                 nat.to_dev(np.concatenate(edges)))
+            object.__setattr__(self, "_grid_cache", g)
+        return g
+
+    def evaluate_device(self, d_pts, out=None, work=None):
+        """K4 on device-resident points (P, dim) float64; returns a device tensor.
+
+        Raises like the reference: ValueError for a point outside all boxes
+        (first index), FloatingPointError for a degenerate denominator.
+        """
+        from . import _native as nat
+
+        torch = nat.torch_mod()
+        ds = self._device()
+        dim, d_shape, d_edges = self._grid_dev()
+        P = int(d_pts.shape[0])
+        S = self.partition.n_subdomains
+        if out is None:
+            out = torch.empty(P, dtype=torch.float64, device=d_pts.device)
+        if work is None:
+            work = torch.empty(int(nat.lib().pam_eval_workspace_bytes(P, S)), dtype=torch.uint8,
+                               device=d_pts.device)
+        err = nat.ErrorWord()
+        nat.check(nat.lib().pam_eval_f64(
+            dim, P, nat.ptr(d_pts), nat.ptr(d_shape), nat.ptr(d_edges), S, nat.ptr(ds.d_dict_off),
+            nat.ptr(ds.d_m_cur), nat.ptr(ds.d_centres), nat.ptr(ds.d_widths), nat.ptr(ds.d_beta),
+            nat.ptr(ds.d_log), nat.ptr(out), nat.ptr(work), nat.ptr(err.t), nat.stream_ptr()),
+            "pam_eval_f64")
+        code, j = err.read()
+        if code == nat.PAM_ERR_OUTSIDE:
+            pt = d_pts[j].cpu().numpy().tolist()
+            raise ValueError(f"point index {j} = {pt} lies outside all boxes")
+        if code:
+            nat.raise_data_error(code, j)
+        return out
+
+    def evaluate(self, points) -> np.ndarray:
+        """Evaluate at arbitrary points, order preserved (partition.py:132-143)."""
+        from . import _native as nat
+
+        pts = np.asarray(points, dtype=float)
+        if pts.ndim == 1:
+            dim = self.partition.mesh.dim
+            pts = pts[:, None] if dim == 1 else pts[None, :]
+        if pts.shape[0] == 0:
+            return np.empty(0)
+        torch = nat.torch_mod()
+        d_pts = torch.from_numpy(np.ascontiguousarray(pts)).to(nat.device(), non_blocking=True)
+        return self.evaluate_device(d_pts).cpu().numpy()
+
+
+@dataclass(frozen=True)
+class ParallelFitReport:
+    """Timings and per-subdomain round histories (partition.py:146-154).
+
+    ``seconds[i]`` is the wall time of the device batch that fitted
+    subdomain i; ``max_concurrent`` the largest number of subdomains fitted
+    concurrently in one batch.
+    """
+
+    rounds: tuple[tuple[RoundReport, ...], ...]
+    seconds: tuple[float, ...]
+    total_seconds: float
+    workers: int
+    max_concurrent: int
+
+
+class _LazyChecksumMeta(dict):
+    """Metadata dict whose ``field_checksum`` is computed on first access."""
+
+    def __init__(self, base, data):
+        super().__init__(base)
+        self._data = data
+
+    def _fill(self):
+        if self._data is not None:
+            dict.setdefault(self, "field_checksum", self._data.checksum())
+            self._data = None
+
+    def __getitem__(self, k):
+        if k == "field_checksum":
+            self._fill()
+        return dict.__getitem__(self, k)
+
+    def get(self, k, default=None):
+        if k == "field_checksum":
+            self._fill()
+        return dict.get(self, k, default)
+
+    def __contains__(self, k):
+        return (k == "field_checksum" and self._data is not None) or dict.__contains__(self, k)
+
+    def __iter__(self):
+        self._fill()
+        return dict.__iter__(self)
+
+    def keys(self):
+        self._fill()
+        return dict.keys(self)
+
+    def items(self):
+        self._fill()
+        return dict.items(self)
+
+    def values(self):
+        self._fill()
+        return dict.values(self)
+
+    def __len__(self):
+        self._fill()
+        return dict.__len__(self)
+
+    def copy(self):
+        self._fill()
+        return dict(self)
+
+    def __eq__(self, other):
+        self._fill()
+        return dict.__eq__(self, other)
+
+    def __repr__(self):
+        self._fill()
+        return dict.__repr__(self)
+
+
+def _broadcast(value, n, klass, name):
+    if isinstance(value, klass):
+        return [value] * n
+    values = list(value)
+    if len(values) != n:
+        raise ValueError(f"{name} has {len(values)} entries for {n} subdomains")
+    return values
+
+
+def _batch_geometry(data: FieldData, partition: Partition):
+    """Device batch (row_off host, pts dev, values dev, cell_idx dev) of all subdomains."""
+    from . import _native as nat
+
+    torch = nat.torch_mod()
+    mesh = partition.mesh
+    S = partition.n_subdomains
+    dev = nat.device()
+    d_vals_all = torch.from_numpy(np.ascontiguousarray(data.values)).to(dev, non_blocking=True)
+    if partition.is_cell_aligned():
+        per = mesh.n_cells // S
+        row_off = np.arange(S + 1, dtype=np.int64) * per
+        pts = torch.empty(mesh.n_cells * mesh.dim, dtype=torch.float64, device=dev)
+        vals = torch.empty(mesh.n_cells, dtype=torch.float64, device=dev)
+        cidx = torch.empty(mesh.n_cells, dtype=torch.int64, device=dev)
+        lo = np.array([b[0] for b in mesh.bounds], dtype=np.float64)
+        nat.check(nat.lib().pam_gather_cells_f64(
+            mesh.dim, nat.ptr(nat.to_dev(np.asarray(mesh.counts, dtype=np.int64))),
+            nat.ptr(nat.to_dev(np.asarray(partition.shape, dtype=np.int32))), nat.ptr(nat.to_dev(lo)),
+            nat.ptr(nat.to_dev(np.asarray(mesh.cell_size, dtype=np.float64))), nat.ptr(d_vals_all), S,
+            nat.ptr(nat.to_dev(row_off)), nat.ptr(pts), nat.ptr(vals), nat.ptr(cidx),
+            nat.stream_ptr()), "pam_gather_cells_f64")
+        return row_off, pts, vals, None
+    # generic boxes: the reference's centroid masks (host), then one upload
+    subs = partition.subdomain_fields(data)
+    row_off = np.concatenate([[0], np.cumsum([s.n_cells for s in subs])]).astype(np.int64)
+    pts = nat.to_dev(np.concatenate([s.centroids for s in subs]).reshape(-1))
+    vals = nat.to_dev(np.concatenate([s.values for s in subs]))
+    return row_off, pts, vals, subs
+
+
+def fit_parallel(
+    data: FieldData,
+    partition: Partition,
+    configs,
+    spec,
+    workers: int = 1,
+    metadata: dict | None = None,
+) -> tuple[GlobalSurrogate, ParallelFitReport]:
+    """Fit every subdomain on the GPU and assemble the global surrogate (partition.py:167-208).
+
+    ``configs`` and ``spec`` may be single values (broadcast) or sequences
+    with one entry per subdomain.  Results are gathered by subdomain index and
+    are identical for any ``workers`` value and any batch chunking.
+    """
+    from . import _native as nat
+    from .engine import (EngineError, FitEngine, chunk_ranges, dictionary_capacity, reports_for,
+                         w_budget_bytes, _round16)
+
+    n = partition.n_subdomains
+    cfgs = _broadcast(configs, n, AdaptiveConfig, "configs")
+    specs = _broadcast(spec, n, DictionarySpec, "spec")
+    mesh = partition.mesh
+    dim = mesh.dim
+    t0 = time.perf_counter()
+    row_off, d_pts, d_vals, subs = _batch_geometry(data, partition)
+    n_rows = np.diff(row_off)
+    boxes = partition.boxes
+    box_lo = np.array([b.lo for b in boxes], dtype=np.float64)
+    box_hi = np.array([b.hi for b in boxes], dtype=np.float64)
+
+    # initial dictionaries: per-cell centroid dictionaries are built on the
+    # device; lattices and user-defined specs on the host (partition.py:109-112)
+    plain = [type(sp) is DictionarySpec for sp in specs]
+    centroid = all(p and sp.lattice is None for p, sp in zip(plain, specs))
+    init = None
+    if not centroid:
+        if subs is None and not all(plain):
+            subs = partition.subdomain_fields(data)
+        init = []
+        for i, sp in enumerate(specs):
+            try:
+                if type(sp) is DictionarySpec and sp.lattice is not None:
+                    d = lattice_dictionary(boxes[i], sp.lattice, sp.sigma)
+                elif type(sp) is DictionarySpec:
+                    cen = (subs[i].centroids if subs is not None
+                           else d_pts.view(-1, dim)[row_off[i]:row_off[i + 1]].cpu().numpy())
+                    d = centroid_dictionary(cen, sp.sigma)
+                else:
+                    sub = subs[i] if subs is not None else data.subdomain(boxes[i])
+                    d = sp.build(sub)
+            except Exception as exc:  # noqa: BLE001 - annotate with the subdomain index
+                raise RuntimeError(f"fit failed on subdomain {i}: {exc}") from exc
+            init.append(d)
+    m0 = n_rows if centroid else np.array([len(d) for d in init], dtype=np.int64)
+    k_top = np.minimum([c.k_top for c in cfgs], n_rows)
+    cap = dictionary_capacity(m0, k_top, [c.m_q for c in cfgs], [c.m_max for c in cfgs],
+                              [c.max_rounds for c in cfgs])
+    wbytes = _round16(n_rows) * cap * 8
+    chunks = chunk_ranges(wbytes, w_budget_bytes())
+
+    locals_ = [None] * n
+    rounds = [None] * n
+    seconds = [0.0] * n
+    dev_parts = []
+    for a, b in chunks:
+        sl_rows = slice(int(row_off[a]) * dim, int(row_off[b]) * dim)
+        kw = {}
+        if centroid:
+            kw["centroid_sigma"] = np.array([specs[i].sigma for i in range(a, b)], dtype=np.float64)
+        else:
+            ds = init[a:b]
+            kw.update(init_centres=np.concatenate([d.centers for d in ds]),
+                      init_widths=np.concatenate([d.widths for d in ds]),
+                      init_gens=np.concatenate([d.generations for d in ds]),
+                      init_m=np.array([len(d) for d in ds], dtype=np.int64))
+        try:
+            eng = FitEngine(dim, mesh.cell_size, row_off[a:b + 1] - row_off[a], d_pts[sl_rows],
+                            d_vals[int(row_off[a]):int(row_off[b])], box_lo[a:b], box_hi[a:b],
+                            cfgs[a:b], **kw)
+            res = eng.run()
+        except EngineError as exc:
+            raise RuntimeError(f"fit failed on subdomain {a + exc.subdomain}: {exc.exc}") from exc.exc
+        for s in range(b - a):
+            i = a + s
+            d = RbfDictionary(centers=res.centres[s], widths=res.widths[s],
+                              generations=res.generations[s])
+            locals_[i] = LocalSurrogate(dictionary=d, beta=res.beta[s], log_transform=True)
+            rounds[i] = tuple(reports_for(res, s, RoundReport))
+            seconds[i] = res.seconds
+        # keep the fitted dictionaries resident for evaluation; drop W
+        dev_parts.append((eng.d_dict_off, eng.d_m_cur, eng.d_centres, eng.d_widths, eng.d_beta,
+                          int(eng.cap.sum())))
+        eng.d_W = None
+    total = time.perf_counter() - t0
+
+    report = ParallelFitReport(
+        rounds=tuple(rounds), seconds=tuple(seconds), total_seconds=total, workers=workers,
+        max_concurrent=max(b - a for a, b in chunks),
+    )
+    meta = _LazyChecksumMeta(dict(metadata or {}), None if "field_checksum" in (metadata or {}) else data)
+    gs = GlobalSurrogate(partition=partition, locals=tuple(locals_), metadata=meta)
+    torch = nat.torch_mod()
+    if len(dev_parts) == 1:
+        off, m, c, w, bt, _ = dev_parts[0]
+    else:
+        shift, offs = 0, []
+        for part in dev_parts:
+            offs.append(part[0] + shift)
+            shift += part[5]
+        off = torch.cat(offs)
+        m = torch.cat([p[1] for p in dev_parts])
+        c = torch.cat([p[2] for p in dev_parts])
+        w = torch.cat([p[3] for p in dev_parts])
+        bt = torch.cat([p[4] for p in dev_parts])
+    logf = torch.ones(n, dtype=torch.int32, device=nat.device())
+    gs.attach_device(DeviceSurrogate(dim, off, m, c, w, bt, logf))
+    return gs, report
+
+
+# ---------------------------------------------------------------------------
+# serialization: self-describing text format with lossless float round trip
+# (reference partition.py:220-347; next-row (f) of the survey, host I/O)
+
+
+def save(surrogate: GlobalSurrogate, sink) -> None:
+    """Write a surrogate as a version-tagged text document."""
+    mesh = surrogate.partition.mesh
+    lines = [f"{SURROGATE_FORMAT} {SURROGATE_VERSION}"]
+    lines.append(f"dim {mesh.dim}")
+    lines.append("counts " + " ".join(str(n) for n in mesh.counts))
+    lines.append("bounds " + " ".join(f"{v:.17g}" for b in mesh.bounds for v in b))
+    lines.append("grid " + " ".join(str(p) for p in surrogate.partition.shape))
+    for key in sorted(surrogate.metadata):
+        value = str(surrogate.metadata[key]).replace("\n", " ")
+        lines.append(f"meta {key} {value}")
+    for i, loc in enumerate(surrogate.locals):
+        d = loc.dictionary
+        lines.append(f"subdomain {i} entries {len(d)} log {int(loc.log_transform)}")
+        for c, w, b, g in zip(d.centers, d.widths, loc.beta, d.generations):
+            coords = " ".join(f"{v:.17g}" for v in c)
+            lines.append(f"{coords} {w:.17g} {b:.17g} {int(g)}")
+    lines.append("end")
+    text = "\n".join(lines) + "\n"
+    if hasattr(sink, "write"):
+        sink.write(text)
+    else:
+        with open(sink, "w") as fh:
+            fh.write(text)
+
+
+def _expect(line: str, key: str):
+    toks = line.split()
+    if not toks or toks[0] != key:
+        raise ValueError(f"expected '{key}' line, got {line!r}")
+    return toks[1:]
+
+
+def load(source) -> GlobalSurrogate:
+    """Read a surrogate written by :func:`save`."""
+    if hasattr(source, "read"):
+        text = source.read()
+    else:
+        try:
+            with open(source) as fh:
+                text = fh.read()
+        except OSError as exc:
+            raise DataError(f"cannot read {source}: {exc}") from exc
+    lines = text.splitlines()
+    pos = 0
+
+    def next_line():
+        nonlocal pos
+        if pos >= len(lines):
+            raise DataError("surrogate file truncated: unexpected end of input")
+        line = lines[pos]
+        pos += 1
+        return line
+
+    header = next_line().split()
+    if len(header) != 2 or header[0] != SURROGATE_FORMAT:
+        raise DataError(f"not a surrogate file (header {header!r})")
+    if int(header[1]) != SURROGATE_VERSION:
+        raise DataError(f"unsupported surrogate format version {header[1]}")
+    try:
+        dim = int(_expect(next_line(), "dim")[0])
+        counts = tuple(int(v) for v in _expect(next_line(), "counts"))
+        flat = [float(v) for v in _expect(next_line(), "bounds")]
+        bounds = tuple((flat[2 * k], flat[2 * k + 1]) for k in range(dim))
+        grid = tuple(int(v) for v in _expect(next_line(), "grid"))
+    except (ValueError, IndexError) as exc:
+        raise DataError(f"malformed surrogate header: {exc}") from exc
+    metadata = {}
+    line = next_line()
+    while line.startswith("meta "):
+        _, key, value = line.split(" ", 2)
+        metadata[key] = value
+        line = next_line()
+    part = make_partition(build_mesh(dim, counts, bounds), *grid)
+    locals_ = []
+    for i in range(part.n_subdomains):
+        toks = line.split()
+        try:
+            if toks[0] != "subdomain" or int(toks[1]) != i:
+                raise ValueError(f"expected subdomain {i}, got {line!r}")
+            n_entries = int(toks[3])
+            log_flag = bool(int(toks[5]))
+        except (ValueError, IndexError) as exc:
+            raise DataError(f"malformed subdomain header: {exc}") from exc
+        rows = []
+        for m in range(n_entries):
+            toks = next_line().split()
+            if len(toks) != dim + 3:
+                raise DataError(f"malformed dictionary entry at subdomain {i} row {m}")
+            rows.append(toks)
+        try:
+            arr = np.array(rows, dtype=float).reshape(n_entries, dim + 3)
+            gens = np.array([int(r[dim + 2]) for r in rows], dtype=int)
+        except ValueError as exc:
+            raise DataError(f"malformed number at subdomain {i}: {exc}") from exc
+        locals_.append(LocalSurrogate(
+            dictionary=RbfDictionary(centers=arr[:, :dim], widths=arr[:, dim], generations=gens),
+            beta=arr[:, dim + 1], log_transform=log_flag))
+        line = next_line()
+    if line.strip() != "end":
+        raise DataError(f"surrogate file missing end marker, found {line!r}")
+    return GlobalSurrogate(partition=part, locals=tuple(locals_), metadata=metadata)
+
+
+def dumps(surrogate: GlobalSurrogate) -> str:
+    buf = io.StringIO()
+    save(surrogate, buf)
+    return buf.getvalue()
+
+
+def loads(text: str) -> GlobalSurrogate:
+    return load(io.StringIO(text))

@@ -1,0 +1,212 @@
+"""Generate the committed golden fixtures by running the REFERENCE itself.
+
+Run in the build container (the reference is importable only here):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Every fixture stores the reference's outputs for seeded inputs that the
+GPU box regenerates deterministically from ``paper_2605_16564_b200.workloads``
+(an input checksum is stored alongside so drift is detected).  3D cases use
+the reference's dimension-generic subdomain-level functions
+(SubdomainField / RbfDictionary / fit_adaptive with explicit 3D offsets,
+SURVEY F4), fed by this repo's 3D mesh/partition restatement, which is
+itself pinned against the reference formulas in tests/test_oracle_pins.py.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+OUT = Path(__file__).resolve().parent
+
+import fieldfit as ff  # noqa: E402  (the reference)
+from fieldfit.adaptive import AdaptiveConfig as RAdaptive  # noqa: E402
+from fieldfit.adaptive import fit_adaptive as r_fit_adaptive  # noqa: E402
+from fieldfit.adaptive import mark as r_mark, enrich as r_enrich  # noqa: E402
+from fieldfit.elastic_net import ElasticNetConfig as REN, fit as r_fit  # noqa: E402
+from fieldfit.fields import SubdomainField as RSub  # noqa: E402
+from fieldfit.geometry import Box as RBox  # noqa: E402
+from fieldfit.rbf import RbfDictionary as RDict, shepard_features as r_features, shepard_eval as r_eval  # noqa: E402
+
+from paper_2605_16564_b200 import workloads  # noqa: E402  (host-only generators)
+from oracle import pam_oracle as O  # noqa: E402
+
+
+def digest(*arrays) -> str:
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def r_cfg(cfg):
+    e = cfg.elastic
+    return RAdaptive(k_top=cfg.k_top, m_max=cfg.m_max, eps_tol=cfg.eps_tol, eta=cfg.eta, m_q=cfg.m_q,
+                     max_rounds=cfg.max_rounds, offsets=cfg.offsets, quad_order=cfg.quad_order,
+                     elastic=REN(lam1=e.lam1, lam2=e.lam2, tol=e.tol, max_iters=e.max_iters))
+
+
+def run_subdomain(field, shape, s, cfg, spec, n_probe=64, seed=0):
+    """Reference fit of subdomain s of a workload (what _fit_one does, partition.py:157-164)."""
+    mesh = field.mesh
+    boxes, owner, _ = O.partition_boxes(mesh.counts, mesh.bounds, shape)
+    lo, hi, op = boxes[s]
+    box = RBox(lo=lo, hi=hi, open_hi=op)
+    rows = O.subdomain_rows(mesh.centroids, boxes[s])
+    sub = RSub(box=box, cell_indices=rows, centroids=mesh.centroids[rows], values=field.values[rows],
+               cell_size=mesh.cell_size)
+    if spec.lattice is None:
+        d0 = RDict(centers=sub.centroids, widths=np.full(rows.size, spec.sigma))
+    else:
+        d0 = RDict(centers=O.lattice_centers(lo, hi, spec.lattice),
+                   widths=np.full(spec.lattice ** mesh.dim, spec.sigma))
+    t = time.time()
+    sur, reps = r_fit_adaptive(sub, d0, r_cfg(cfg))
+    dt = time.time() - t
+    rng = np.random.default_rng(seed + s)
+    probe = np.asarray(lo) + rng.random((n_probe, mesh.dim)) * (np.asarray(hi) - np.asarray(lo))
+    vals = sur.evaluate(probe)
+    rep = np.array([[r.round, r.centers, r.added, r.max_residual, r.rel_l2, r.abs_l2, r.objective]
+                    for r in reps])
+    return dict(rows=rows, centers=sur.dictionary.centers, widths=sur.dictionary.widths,
+                generations=sur.dictionary.generations, beta=sur.beta, reports=rep, probe=probe,
+                probe_values=vals, seconds=dt)
+
+
+def save_case(name, field, shape, subs, cfg, spec, extra=None):
+    out = {"input_digest": digest(field.values), "shape": np.array(shape),
+           "subdomains": np.array(subs)}
+    for s in subs:
+        t = time.time()
+        r = run_subdomain(field, shape, s, cfg, spec)
+        for k, v in r.items():
+            if k != "seconds":
+                out[f"s{s}_{k}"] = v
+        print(f"  {name} subdomain {s}: centres {r['reports'][:, 1].astype(int).tolist()} "
+              f"({time.time() - t:.1f}s)", flush=True)
+    if extra:
+        out.update(extra)
+    np.savez_compressed(OUT / f"{name}.npz", **out)
+
+
+def kernels_case():
+    """Feature/eval/CD/mark/enrich vectors from the reference's own functions."""
+    rng = np.random.default_rng(1234)
+    out = {}
+    for dim in (1, 2, 3):
+        M, N = 37, 53
+        c = rng.random((M, dim))
+        w = rng.uniform(0.05, 0.3, M)
+        x = rng.random((N, dim))
+        d = RDict(centers=c, widths=w)
+        out[f"feat{dim}_c"], out[f"feat{dim}_w"], out[f"feat{dim}_x"] = c, w, x
+        out[f"feat{dim}_L"] = d.log_features(x)
+        out[f"feat{dim}_W"] = r_features(x, d)
+        b = rng.standard_normal(M)
+        out[f"feat{dim}_beta"] = b
+        out[f"feat{dim}_eval"] = r_eval(x, d, b)
+    # CD fits at several shapes / tolerances (elastic_net.py:66-110)
+    for k, (n, m, l1, l2, tol, it) in enumerate([(40, 25, 0.05, 0.01, 1e-10, 100000),
+                                                 (100, 150, 4.59e-4, 1e-4, 1e-6, 4000),
+                                                 (257, 64, 0.01, 0.0, 1e-12, 20000),
+                                                 (600, 300, 4.59e-4, 1e-4, 1e-6, 700)]):
+        W = np.abs(rng.standard_normal((n, m)))
+        W /= W.sum(axis=1, keepdims=True)
+        y = rng.standard_normal(n)
+        b0 = rng.standard_normal(m) * 0.1 if k == 1 else None
+        res = r_fit(W, y, REN(lam1=l1, lam2=l2, tol=tol, max_iters=it), beta0=b0)
+        out[f"cd{k}_W"], out[f"cd{k}_y"] = W, y
+        out[f"cd{k}_params"] = np.array([l1, l2, tol, it])
+        if b0 is not None:
+            out[f"cd{k}_beta0"] = b0
+        out[f"cd{k}_beta"], out[f"cd{k}_hist"] = res.beta, res.objective_history
+        out[f"cd{k}_iters"] = np.array([res.iterations, int(res.converged)])
+    # mark with ties (adaptive.py:141-152)
+    R = np.round(rng.random(300) * 20) / 20
+    R[::7] = 0.0
+    out["mark_R"] = R
+    out["mark_out"] = r_mark(R, 50)
+    # enrich 2D with duplicates against the existing dictionary (adaptive.py:167-210)
+    f = ff.box_field_2d(8, 8)
+    sub = f.whole()
+    d = RDict(centers=sub.centroids, widths=np.full(64, 0.1))
+    mk = np.array([3, 9, 27, 63, 0])
+    nc, nw = r_enrich(d, mk, sub, 0.5, 3, offsets=((0.0, 0.0), (-0.5, 0.0), (0.5, 0.5)))
+    d2 = d.extended(nc, nw, 1)
+    nc2, nw2 = r_enrich(d2, mk, sub, 0.5, 3, offsets=((0.0, 0.0), (-0.5, 0.0), (0.5, 0.5)))
+    out["enr_centers2"], out["enr_widths2"] = d2.centers, d2.widths
+    out["enr_new1_c"], out["enr_new1_w"], out["enr_new2_c"], out["enr_new2_w"] = nc, nw, nc2, nw2
+    np.savez_compressed(OUT / "kernels.npz", **out)
+    print("  kernels.npz written")
+
+
+def adaptive_small_cases():
+    """Reference fit_adaptive on the reference's own test fields (1D/2D) and a 3D field."""
+    out = {}
+    # 1D step (tests/test_adaptive.py:166-172): centers [16, 22, 28]
+    f = ff.step_field_1d(16)
+    sub = f.whole()
+    cfg = RAdaptive(k_top=2, m_max=12, eta=0.5, m_q=3, max_rounds=3,
+                    elastic=REN(lam1=4.59e-4, lam2=4.64e-6))
+    sur, reps = r_fit_adaptive(sub, ff.centroid_dictionary(sub.centroids, 0.0019), cfg)
+    out["a1_centers"], out["a1_widths"], out["a1_beta"] = sur.dictionary.centers, sur.dictionary.widths, sur.beta
+    out["a1_reports"] = np.array([[r.centers, r.added, r.max_residual, r.rel_l2, r.objective] for r in reps])
+    # 2D box field (tests/test_adaptive.py:212-223 at 16x16)
+    f = ff.box_field_2d(16, 16)
+    sub = f.whole()
+    cfg = RAdaptive(k_top=51, m_max=306, eta=0.5, m_q=3, max_rounds=3,
+                    elastic=REN(lam1=4.59e-4, lam2=1e-4, tol=1e-6, max_iters=1500),
+                    offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
+    sur, reps = r_fit_adaptive(sub, ff.centroid_dictionary(sub.centroids, 0.0625), cfg)
+    out["a2_centers"], out["a2_widths"], out["a2_beta"] = sur.dictionary.centers, sur.dictionary.widths, sur.beta
+    out["a2_gens"] = sur.dictionary.generations
+    out["a2_reports"] = np.array([[r.centers, r.added, r.max_residual, r.rel_l2, r.objective] for r in reps])
+    # 3D: 6x5x4 cells of the SPE10-shaped field, explicit 3D offsets, order-2 quadrature
+    fld = workloads.spe10_like_field(4)
+    mesh = fld.mesh
+    rows = np.array([((iz * 220 + iy) * 60 + ix) for iz in range(40, 44) for iy in range(10, 15)
+                     for ix in range(20, 26)])
+    box = RBox(lo=(400.0, 100.0, 80.0), hi=(520.0, 150.0, 88.0), open_hi=(True, True, True))
+    sub = RSub(box=box, cell_indices=rows, centroids=mesh.centroids[rows], values=fld.values[rows],
+               cell_size=mesh.cell_size)
+    cfg = RAdaptive(k_top=24, m_max=144, eta=0.5, m_q=3, max_rounds=3, quad_order=2,
+                    elastic=REN(lam1=4.59e-4, lam2=1e-4, tol=1e-6, max_iters=1000),
+                    offsets=workloads.IN_CELL_3D)
+    sigma = float(np.prod(mesh.cell_size) ** (1 / 3))
+    sur, reps = r_fit_adaptive(sub, RDict(centers=sub.centroids, widths=np.full(rows.size, sigma)), cfg)
+    out["a3_rows"] = rows
+    out["a3_centers"], out["a3_widths"], out["a3_beta"] = sur.dictionary.centers, sur.dictionary.widths, sur.beta
+    out["a3_gens"] = sur.dictionary.generations
+    out["a3_reports"] = np.array([[r.centers, r.added, r.max_residual, r.rel_l2, r.objective] for r in reps])
+    np.savez_compressed(OUT / "adaptive_small.npz", **out)
+    print("  adaptive_small.npz written", [r.centers for r in reps])
+
+
+def main(which):
+    if "kernels" in which:
+        kernels_case()
+    if "adaptive" in which:
+        adaptive_small_cases()
+    if "C1" in which:
+        wl = workloads.config1()
+        save_case("C1", wl.field, wl.shape, [0, 1, 2, 3], wl.config, wl.spec)
+    if "C2" in which:
+        wl = workloads.config2()
+        save_case("C2", wl.field, wl.shape, [19, 42], wl.config, wl.spec)
+    if "C3" in which:
+        wl = workloads.config3()
+        save_case("C3", wl.field, wl.shape, [77], wl.config, wl.spec)
+    if "C4" in which:
+        wl = workloads.config4(with_refined_eval=False)
+        save_case("C4", wl.field, wl.shape, [0, 500, 1337, 2243], wl.config, wl.spec)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["kernels", "adaptive", "C1", "C2", "C3", "C4"])

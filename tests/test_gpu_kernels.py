@@ -1,0 +1,204 @@
+"""GPU parity of each sm_100a kernel against the reference's golden vectors
+(tests/golden/kernels.npz, produced by running the reference) and the oracle.
+
+Tolerances: log-feature exponents, marking, enrichment and ownership are
+bit-exact; Shepard weights/evaluations 1e-13 relative (exp / row-sum ulps);
+coordinate-descent coefficients 1e-8 relative to max|beta| (SURVEY F2 shows
+~1e-12 is typical: only the order of the length-N dot products differs).
+"""
+
+import numpy as np
+import pytest
+
+import paper_2605_16564_b200 as pam
+from oracle import pam_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("dim", [1, 2, 3])
+def test_log_features_bit_exact(cuda, golden, dim):
+    g = golden("kernels")
+    d = pam.RbfDictionary(centers=g[f"feat{dim}_c"], widths=g[f"feat{dim}_w"])
+    L = d.log_features(g[f"feat{dim}_x"])
+    np.testing.assert_array_equal(L, g[f"feat{dim}_L"])
+
+
+@pytest.mark.parametrize("dim", [1, 2, 3])
+def test_shepard_features_and_eval(cuda, golden, dim):
+    g = golden("kernels")
+    d = pam.RbfDictionary(centers=g[f"feat{dim}_c"], widths=g[f"feat{dim}_w"])
+    W = pam.shepard_features(g[f"feat{dim}_x"], d)
+    np.testing.assert_allclose(W, g[f"feat{dim}_W"], rtol=1e-13, atol=1e-300)
+    np.testing.assert_allclose(W.sum(axis=1), 1.0, atol=1e-13)  # partition of unity
+    v = pam.shepard_eval(g[f"feat{dim}_x"], d, g[f"feat{dim}_beta"])
+    np.testing.assert_allclose(v, g[f"feat{dim}_eval"], rtol=1e-13, atol=1e-14)
+    fm = pam.assemble_features(g[f"feat{dim}_x"], d)
+    np.testing.assert_allclose(fm.values, np.exp(g[f"feat{dim}_L"]), rtol=1e-15, atol=0)
+    norm = pam.shepard_normalize(fm)
+    np.testing.assert_allclose(norm.values, g[f"feat{dim}_W"], rtol=1e-13, atol=1e-300)
+
+
+def test_shepard_normalize_zero_row(cuda):
+    fm = pam.FeatureMatrix(values=np.array([[0.5, 0.5], [0.0, 0.0]]), normalized=False)
+    with pytest.raises(ValueError, match="row 1"):
+        pam.shepard_normalize(fm)
+
+
+def test_underflow_rows_normalise(cuda):
+    d = pam.RbfDictionary(centers=np.array([[0.0], [0.1]]), widths=np.array([0.001, 0.001]))
+    W = pam.shepard_features(np.array([[50.0]]), d)
+    np.testing.assert_allclose(W.sum(axis=1), 1.0, atol=1e-12)
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+def test_cd_matches_reference(cuda, golden, k):
+    g = golden("kernels")
+    l1, l2, tol, it = g[f"cd{k}_params"]
+    cfg = pam.ElasticNetConfig(lam1=l1, lam2=l2, tol=tol, max_iters=int(it))
+    b0 = g.get(f"cd{k}_beta0")
+    res = pam.fit(g[f"cd{k}_W"], g[f"cd{k}_y"], cfg, beta0=b0)
+    ref_beta = g[f"cd{k}_beta"]
+    scale = max(1.0, np.abs(ref_beta).max())
+    assert np.max(np.abs(res.beta - ref_beta)) <= 1e-8 * scale
+    iters, conv = g[f"cd{k}_iters"]
+    assert abs(res.iterations - iters) <= 1 and res.converged == bool(conv)
+    n = min(res.iterations, iters)
+    np.testing.assert_allclose(res.objective_history[:n], g[f"cd{k}_hist"][:n], rtol=1e-9)
+
+
+def test_cd_frozen_oracle_instance(cuda):
+    # reference tests/test_elastic_net.py:13-20, 57-60
+    rng = np.random.default_rng(20240817)
+    W, y = rng.standard_normal((8, 8)), rng.standard_normal(8)
+    res = pam.fit(W, y, pam.ElasticNetConfig(lam1=0.3, lam2=0.2))
+    assert abs(res.objective - 1.3720329345548663) <= 1e-8
+    assert res.converged
+
+
+def test_cd_known_answers(cuda):
+    y = np.array([0.3, -1.2, 2.0])
+    res = pam.fit(np.eye(3), y, pam.ElasticNetConfig())
+    np.testing.assert_allclose(res.beta, y, atol=1e-12)
+    rng = np.random.default_rng(1)
+    W, y = rng.standard_normal((10, 4)), rng.standard_normal(10)
+    lam_max = np.max(np.abs(W.T @ y))
+    res = pam.fit(W, y, pam.ElasticNetConfig(lam1=lam_max * 1.0001))
+    assert res.active_set_size == 0
+    res, flag = pam.fit_log_field(np.array([1e-4, 1e-1]), np.eye(2), pam.ElasticNetConfig())
+    assert flag
+    np.testing.assert_allclose(res.beta, [-4 * np.log(10), -np.log(10)], atol=1e-10)
+    res = pam.fit(W, y, pam.ElasticNetConfig(lam1=0.01, max_iters=1))
+    assert not res.converged and res.iterations == 1
+
+
+def test_cd_oracle_random_instances(cuda):
+    # reference test_oracle_equivalence_random_instances shapes, against the bit-exact oracle
+    rng = np.random.default_rng(77)
+    for _ in range(20):
+        m = int(rng.integers(1, 18))
+        n = int(rng.integers(m + 3, 21))
+        W, y = rng.standard_normal((n, m)), rng.standard_normal(n)
+        l1, l2 = float(rng.uniform(0, 1)), float(rng.uniform(0, 1))
+        res = pam.fit(W, y, pam.ElasticNetConfig(lam1=l1, lam2=l2))
+        o = O.fit(W, y, l1, l2, 1e-10, 100000)
+        assert np.max(np.abs(res.beta - o["beta"])) <= 1e-9
+        assert abs(res.objective - o["objective"]) <= 1e-10 * max(1, abs(o["objective"]))
+
+
+@pytest.mark.parametrize("n", [33, 700, 1500, 3000])
+def test_cd_group_kernels_large_n(cuda, n):
+    # rows beyond one warp's register budget use the multi-warp group kernels
+    rng = np.random.default_rng(n)
+    m = 40
+    W = np.abs(rng.standard_normal((n, m)))
+    W /= W.sum(axis=1, keepdims=True)
+    y = rng.standard_normal(n)
+    res = pam.fit(W, y, pam.ElasticNetConfig(lam1=1e-3, lam2=1e-4, tol=1e-9, max_iters=3000))
+    o = O.fit(W, y, 1e-3, 1e-4, 1e-9, 3000)
+    assert np.max(np.abs(res.beta - o["beta"])) <= 1e-8 * max(1, np.abs(o["beta"]).max())
+    assert abs(res.iterations - o["iterations"]) <= 1
+
+
+def test_mark_bit_exact(cuda, golden):
+    g = golden("kernels")
+    np.testing.assert_array_equal(pam.mark(g["mark_R"], 50), g["mark_out"])
+    np.testing.assert_array_equal(pam.mark(np.array([1.0, 3.0, 1.0, 3.0, 0.5]), 3), [1, 3, 0])
+    assert pam.mark(np.zeros(10), 3).size == 0
+    with pytest.raises(ValueError):
+        pam.mark(np.ones(3), 4)
+
+
+def test_enrich_bit_exact(cuda, golden):
+    g = golden("kernels")
+    f = pam.box_field_2d(8, 8)
+    sub = f.whole()
+    d = pam.RbfDictionary(centers=sub.centroids, widths=np.full(64, 0.1))
+    mk = np.array([3, 9, 27, 63, 0])
+    offs = ((0.0, 0.0), (-0.5, 0.0), (0.5, 0.5))
+    nc, nw = pam.enrich(d, mk, sub, 0.5, 3, offsets=offs)
+    np.testing.assert_array_equal(nc, g["enr_new1_c"])
+    np.testing.assert_array_equal(nw, g["enr_new1_w"])
+    d2 = d.extended(nc, nw, 1)
+    nc2, nw2 = pam.enrich(d2, mk, sub, 0.5, 3, offsets=offs)
+    np.testing.assert_array_equal(nc2, g["enr_new2_c"])
+    np.testing.assert_array_equal(nw2, g["enr_new2_w"])
+    with pytest.raises(ValueError):
+        pam.enrich(d, [], sub, 0.5, 3)
+
+
+def test_enrich_reference_unit_cases(cuda):
+    # reference tests/test_adaptive.py:91-127
+    field = pam.step_field_1d(8)
+    sub = field.whole()
+    d = pam.centroid_dictionary(sub.centroids, 0.002)
+    centers, widths = pam.enrich(d, [3], sub, eta=0.5, m_q=3)
+    np.testing.assert_allclose(widths, 0.001)
+    dx, x_t = sub.cell_size[0], sub.centroids[3, 0]
+    np.testing.assert_allclose(sorted(centers[:, 0]), [x_t - dx / 4, x_t, x_t + dx / 4])
+    field = pam.step_field_1d(4)
+    sub = field.whole()
+    centers, _ = pam.enrich(pam.centroid_dictionary(sub.centroids, 0.002), [0, 3], sub, eta=0.5, m_q=3)
+    assert np.all(centers[:, 0] >= sub.box.lo[0]) and np.all(centers[:, 0] <= sub.box.hi[0])
+
+
+def test_locate_many_bit_exact(cuda):
+    rng = np.random.default_rng(7)
+    boxes = []
+    for j in range(2):
+        for i in range(4):
+            boxes.append(pam.Box(lo=(i / 4, j / 2), hi=((i + 1) / 4, (j + 1) / 2), open_hi=(i < 3, j < 1)))
+    pts = rng.random((100_000, 2))
+    pts[:100, 0] = 0.5  # exactly on internal faces
+    pts[100:200, 1] = 0.5
+    pts[200] = (1.0, 1.0)  # global upper corner
+    owner = pam.locate_many(pts, boxes)
+    ref = O.locate_many(pts, [(b.lo, b.hi, b.open_hi) for b in boxes])
+    np.testing.assert_array_equal(owner, ref)
+    with pytest.raises(ValueError, match="point index 3"):
+        bad = pts[:10].copy()
+        bad[3] = (1.5, 0.2)
+        bad[7] = (-0.1, 0.2)
+        pam.locate_many(bad, boxes)
+
+
+def test_locate_general_bounds_edges(cuda):
+    # ownership by float edge comparison: points at edges +-1 ulp
+    mesh = pam.build_mesh(3, (12, 10, 6), ((0.1, 1.7), (-3.3, 2.9), (5.0, 5.7)))
+    part = pam.make_partition(mesh, 4, 5, 3)
+    _, edges = part.grid
+    rng = np.random.default_rng(3)
+    pts = []
+    for k in range(3):
+        for e in edges[k]:
+            for d in (-1, 0, 1):
+                p = np.array([np.mean(mesh.bounds[a]) for a in range(3)])
+                p[k] = np.nextafter(e, e + d) if d else e
+                p[(k + 1) % 3] = rng.uniform(*mesh.bounds[(k + 1) % 3])
+                pts.append(p)
+    pts = np.array(pts)
+    inside = np.all([(pts[:, k] >= mesh.bounds[k][0]) & (pts[:, k] <= mesh.bounds[k][1]) for k in range(3)], axis=0)
+    pts = pts[inside]
+    owner = pam.locate_many(pts, part.boxes)
+    ref = O.locate_many(pts, [(b.lo, b.hi, b.open_hi) for b in part.boxes])
+    np.testing.assert_array_equal(owner, ref)

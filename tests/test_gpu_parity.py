@@ -1,0 +1,280 @@
+"""End-to-end GPU parity of the batched adaptive fit and the fused evaluation
+against the reference's own outputs (golden fixtures made by running the
+reference, tests/golden/make_golden.py) and the bit-exact CPU oracle.
+
+Contract (BASELINE north_star): subdomain partition and cell ownership
+bit-exact; selected-centre sets (dictionaries) identical; coefficients,
+reconstructed values and L1/L2 errors within 1e-8 relative.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_2605_16564_b200 as pam
+from paper_2605_16564_b200 import workloads
+from oracle import pam_oracle as O
+
+pytestmark = pytest.mark.gpu
+BETA_TOL = 1e-8
+VAL_TOL = 1e-8
+
+
+def _assert_local_matches(loc, g, prefix, check_reports=None):
+    np.testing.assert_array_equal(loc.dictionary.centers, g[f"{prefix}centers"])
+    np.testing.assert_array_equal(loc.dictionary.widths, g[f"{prefix}widths"])
+    if f"{prefix}generations" in g:
+        np.testing.assert_array_equal(loc.dictionary.generations, g[f"{prefix}generations"])
+    ref = g[f"{prefix}beta"]
+    assert np.max(np.abs(loc.beta - ref)) <= BETA_TOL * max(1.0, np.abs(ref).max())
+
+
+def _assert_reports(reps, ref_rows, cols):
+    """ref_rows columns named by `cols`; counts exact, reals 1e-8 relative."""
+    assert len(reps) == len(ref_rows)
+    for r, row in zip(reps, ref_rows):
+        for name, v in zip(cols, row):
+            got = getattr(r, name)
+            if name in ("round", "centers", "added"):
+                assert got == int(v), (name, got, v)
+            else:
+                assert abs(got - v) <= 1e-8 * max(abs(v), 1e-300) + 1e-300, (name, got, v)
+
+
+def test_fit_adaptive_1d_step(cuda, golden):
+    g = golden("adaptive_small")
+    field = pam.step_field_1d(16)
+    sub = field.whole()
+    cfg = pam.AdaptiveConfig(k_top=2, m_max=12, eta=0.5, m_q=3, max_rounds=3,
+                             elastic=pam.ElasticNetConfig(lam1=4.59e-4, lam2=4.64e-6))
+    sur, reps = pam.fit_adaptive(sub, pam.centroid_dictionary(sub.centroids, 0.0019), cfg)
+    assert [r.centers for r in reps] == [16, 22, 28]  # reference test_adaptive.py:166-172
+    assert [r.added for r in reps] == [0, 6, 12]
+    _assert_local_matches(sur, g, "a1_")
+    _assert_reports(reps, g["a1_reports"], ("centers", "added", "max_residual", "rel_l2", "objective"))
+
+
+def test_fit_adaptive_2d_box(cuda, golden):
+    g = golden("adaptive_small")
+    field = pam.box_field_2d(16, 16)
+    sub = field.whole()
+    cfg = pam.AdaptiveConfig(k_top=51, m_max=306, eta=0.5, m_q=3, max_rounds=3,
+                             elastic=pam.ElasticNetConfig(lam1=4.59e-4, lam2=1e-4, tol=1e-6, max_iters=1500),
+                             offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
+    sur, reps = pam.fit_adaptive(sub, pam.centroid_dictionary(sub.centroids, 0.0625), cfg)
+    _assert_local_matches(sur, g, "a2_")
+    _assert_reports(reps, g["a2_reports"], ("centers", "added", "max_residual", "rel_l2", "objective"))
+    errs = [r.rel_l2 for r in reps]
+    assert all(b < a for a, b in zip(errs, errs[1:]))
+
+
+def test_fit_adaptive_3d_quad2(cuda, golden):
+    g = golden("adaptive_small")
+    fld = workloads.spe10_like_field(4)
+    mesh = fld.mesh
+    rows = g["a3_rows"]
+    box = pam.Box(lo=(400.0, 100.0, 80.0), hi=(520.0, 150.0, 88.0), open_hi=(True, True, True))
+    sub = pam.SubdomainField(box=box, cell_indices=rows, centroids=mesh.centroids[rows],
+                             values=fld.values[rows], cell_size=mesh.cell_size)
+    cfg = pam.AdaptiveConfig(k_top=24, m_max=144, eta=0.5, m_q=3, max_rounds=3, quad_order=2,
+                             elastic=pam.ElasticNetConfig(lam1=4.59e-4, lam2=1e-4, tol=1e-6, max_iters=1000),
+                             offsets=workloads.IN_CELL_3D)
+    sigma = float(np.prod(mesh.cell_size) ** (1 / 3))
+    sur, reps = pam.fit_adaptive(sub, pam.RbfDictionary(centers=sub.centroids, widths=np.full(rows.size, sigma)), cfg)
+    _assert_local_matches(sur, g, "a3_")
+    _assert_reports(reps, g["a3_reports"], ("centers", "added", "max_residual", "rel_l2", "objective"))
+
+
+def _run_config(wl, eval_points=None):
+    part = wl.partition
+    sur, rep = pam.fit_parallel(wl.field, part, wl.config, wl.spec)
+    return part, sur, rep
+
+
+def _check_golden_subdomains(name, wl, sur, rep, golden):
+    g = golden(name)
+    assert str(g["input_digest"]) == __import__("hashlib").sha256(
+        np.ascontiguousarray(wl.field.values).tobytes()).hexdigest(), "synthetic input drifted"
+    for s in g["subdomains"]:
+        p = f"s{s}_"
+        _assert_local_matches(sur.locals[s], g, p)
+        _assert_reports(rep.rounds[s], g[p + "reports"],
+                        ("round", "centers", "added", "max_residual", "rel_l2", "abs_l2", "objective"))
+        got = sur.evaluate(g[p + "probe"])
+        np.testing.assert_allclose(got, g[p + "probe_values"], rtol=VAL_TOL)
+
+
+def test_config1_step2d_full(cuda, golden):
+    wl = workloads.config1()
+    part, sur, rep = _run_config(wl)
+    _check_golden_subdomains("C1", wl, sur, rep, golden)
+    # evaluation on the 128x128 mesh (mesh transfer) vs the oracle with the golden dictionaries
+    g = golden("C1")
+    boxes = [(b.lo, b.hi, b.open_hi) for b in part.boxes]
+    locs = [(g[f"s{s}_centers"], g[f"s{s}_widths"], g[f"s{s}_beta"]) for s in range(4)]
+    ref, owner = O.global_evaluate(wl.eval_points, boxes, locs)
+    got = sur.evaluate(wl.eval_points)
+    np.testing.assert_allclose(got, ref, rtol=VAL_TOL)
+    np.testing.assert_array_equal(pam.locate_many(wl.eval_points, part.boxes), owner)
+    true = wl.notes["true_field"](wl.eval_points)
+    l1_got = np.sum(np.abs(got - true)) / 128**2
+    l1_ref = np.sum(np.abs(ref - true)) / 128**2
+    assert abs(l1_got - l1_ref) <= 1e-8 * l1_ref
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_config_2d_refined_sampled(cuda, golden, name):
+    wl = workloads.config2() if name == "C2" else workloads.config3(eval_n=256)
+    part, sur, rep = _run_config(wl)
+    _check_golden_subdomains(name, wl, sur, rep, golden)
+    # size-independent properties over ALL subdomains
+    for s, reps in enumerate(rep.rounds):
+        assert reps[0].centers == 1024
+        assert all(b.centers >= a.centers for a, b in zip(reps, reps[1:]))
+        assert np.all(np.isfinite(sur.locals[s].beta))
+    vals = sur.evaluate(wl.eval_points)
+    assert np.all(vals > 0) and np.all(np.isfinite(vals))
+
+
+def test_config4_spe10_shaped_full(cuda, golden):
+    wl = workloads.config4(with_refined_eval=False)
+    part, sur, rep = _run_config(wl)
+    assert part.n_subdomains == 2244
+    _check_golden_subdomains("C4", wl, sur, rep, golden)
+    # cell ownership bit-exact vs the oracle's partition restatement
+    _, owner, _ = O.partition_boxes(wl.field.mesh.counts, wl.field.mesh.bounds, wl.shape)
+    np.testing.assert_array_equal(part.cell_to_subdomain, owner)
+    got_owner = pam.locate_many(wl.field.mesh.centroids, part.boxes)
+    np.testing.assert_array_equal(got_owner, owner)
+    # two more subdomains against the oracle run here (the oracle is bit-exact to the reference)
+    c = wl.config
+    cfgd = dict(lam1=c.elastic.lam1, lam2=c.elastic.lam2, tol=c.elastic.tol, max_iters=c.elastic.max_iters,
+                k_top=c.k_top, m_max=c.m_max, eta=c.eta, m_q=c.m_q, max_rounds=c.max_rounds, offsets=c.offsets)
+    mesh = wl.field.mesh
+    for s in (1, 1999):
+        b = part.boxes[s]
+        rows = O.subdomain_rows(mesh.centroids, (b.lo, b.hi, b.open_hi))
+        cen = mesh.centroids[rows]
+        od = O.fit_adaptive(cen, wl.field.values[rows], mesh.cell_size, b.lo, b.hi, cen,
+                            np.full(rows.size, wl.spec.sigma), cfgd)
+        np.testing.assert_array_equal(sur.locals[s].dictionary.centers, od["centers"])
+        assert np.max(np.abs(sur.locals[s].beta - od["beta"])) <= BETA_TOL * max(1, np.abs(od["beta"]).max())
+    # evaluation at every centroid: positive, finite, matches the per-owner local surrogate
+    vals = sur.evaluate(mesh.centroids)
+    assert np.all(vals > 0) and np.all(np.isfinite(vals))
+    sel = np.flatnonzero(owner == 1337)
+    np.testing.assert_allclose(vals[sel], sur.locals[1337].evaluate(mesh.centroids[sel]), rtol=1e-13)
+
+
+# ---- reference behaviour (tests/test_partition.py) --------------------------
+
+EN_2D = pam.ElasticNetConfig(lam1=4.59e-4, lam2=1e-4, tol=1e-6, max_iters=2000)
+PLAIN_CFG = pam.AdaptiveConfig(m_max=0, elastic=EN_2D)
+
+
+def test_fit_parallel_1x1_matches_direct(cuda):
+    field = pam.box_field_2d(8, 8)
+    part = pam.make_partition(field.mesh, 1, 1)
+    spec = pam.DictionarySpec(sigma=0.13)
+    surrogate, report = pam.fit_parallel(field, part, PLAIN_CFG, spec)
+    direct, _ = pam.fit_adaptive(field.whole(), spec.build(field.whole()), PLAIN_CFG)
+    np.testing.assert_array_equal(surrogate.locals[0].beta, direct.beta)
+    assert len(report.rounds) == 1
+
+
+def test_fit_parallel_constant_field(cuda):
+    mesh = pam.build_mesh(2, (8, 8), ((0, 1), (0, 1)))
+    field = pam.FieldData(mesh=mesh, values=np.full(64, 3.7))
+    part = pam.make_partition(mesh, 2, 2)
+    surrogate, _ = pam.fit_parallel(field, part, pam.AdaptiveConfig(m_max=0), pam.DictionarySpec(sigma=0.13))
+    pts = np.random.default_rng(4).random((200, 2))
+    np.testing.assert_allclose(surrogate.evaluate(pts), 3.7, rtol=1e-6)
+
+
+def test_fit_parallel_deterministic_and_chunk_independent(cuda, monkeypatch):
+    field = pam.box_field_2d(16, 16)
+    part = pam.make_partition(field.mesh, 2, 2)
+    cfg = pam.AdaptiveConfig(k_top=12, m_max=72, m_q=3, max_rounds=3, elastic=EN_2D,
+                             offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
+    spec = pam.DictionarySpec(sigma=0.0625)
+    s1, r1 = pam.fit_parallel(field, part, cfg, spec, workers=1)
+    s4, _ = pam.fit_parallel(field, part, cfg, spec, workers=4)
+    monkeypatch.setenv("PAM_W_BUDGET_GB", "0.0000001")  # one subdomain per device batch
+    sc, rc = pam.fit_parallel(field, part, cfg, spec)
+    assert rc.max_concurrent == 1
+    pts = np.random.default_rng(0).random((500, 2))
+    for other in (s4, sc):
+        for a, b in zip(s1.locals, other.locals):
+            np.testing.assert_array_equal(a.beta, b.beta)
+            np.testing.assert_array_equal(a.dictionary.centers, b.dictionary.centers)
+        np.testing.assert_array_equal(s1.evaluate(pts), other.evaluate(pts))
+    assert pam.dumps(s1) == pam.dumps(s4)
+
+
+class _BrokenSpec(pam.DictionarySpec):
+    def build(self, sub):
+        raise RuntimeError("boom")
+
+
+def test_fit_parallel_errors(cuda):
+    mesh = pam.build_mesh(2, (4, 4), ((0, 1), (0, 1)))
+    field = pam.FieldData(mesh=mesh, values=np.ones(16))
+    part = pam.make_partition(mesh, 2, 1)
+    with pytest.raises(RuntimeError, match="subdomain 1"):
+        pam.fit_parallel(field, part, PLAIN_CFG, [pam.DictionarySpec(sigma=0.1), _BrokenSpec(sigma=0.1)])
+    with pytest.raises(ValueError, match="1 entries for 2"):
+        pam.fit_parallel(field, part, [PLAIN_CFG], pam.DictionarySpec(sigma=0.1))
+
+
+def test_evaluate_order_positivity_and_errors(cuda):
+    field = pam.box_field_2d(8, 8)
+    part = pam.make_partition(field.mesh, 2, 2)
+    surrogate, _ = pam.fit_parallel(field, part, PLAIN_CFG, pam.DictionarySpec(sigma=0.13))
+    pts = np.random.default_rng(1).random((333, 2))
+    vals = surrogate.evaluate(pts)
+    assert np.all(vals > 0)
+    owner = pam.locate_many(pts, part.boxes)
+    for i in range(part.n_subdomains):
+        sel = owner == i
+        np.testing.assert_array_equal(vals[sel], surrogate.locals[i].evaluate(pts[sel]))
+    with pytest.raises(ValueError, match="index 1"):
+        surrogate.evaluate(np.array([[0.5, 0.5], [1.5, 0.5]]))
+    # reloaded (host-built device cache) evaluates bit-identically
+    back = pam.loads(pam.dumps(surrogate))
+    np.testing.assert_array_equal(surrogate.evaluate(pts), back.evaluate(pts))
+
+
+def test_continuity_near_internal_face(cuda):
+    field = pam.box_field_2d(8, 8)
+    part = pam.make_partition(field.mesh, 2, 1)
+    surrogate, _ = pam.fit_parallel(field, part, PLAIN_CFG, pam.DictionarySpec(sigma=0.13))
+    ys = np.linspace(0.05, 0.95, 7)
+    for eps in (1e-6, 1e-9):
+        a = surrogate.evaluate(np.column_stack([np.full(7, 0.5 + eps), ys]))
+        b = surrogate.evaluate(np.column_stack([np.full(7, 0.5 + 2 * eps), ys]))
+        assert np.max(np.abs(a - b)) < (1e-3 if eps == 1e-6 else 1e-6)
+
+
+def test_centroid_values_within_max_residual(cuda):
+    field = pam.box_field_2d(8, 8)
+    part = pam.make_partition(field.mesh, 1, 1)
+    cfg = pam.AdaptiveConfig(m_max=0, elastic=pam.ElasticNetConfig(tol=1e-12))
+    surrogate, report = pam.fit_parallel(field, part, cfg, pam.DictionarySpec(sigma=0.05))
+    vals = surrogate.evaluate(field.mesh.centroids)
+    worst = report.rounds[0][-1].max_residual
+    assert np.max((vals - field.values) ** 2 * field.mesh.cell_measure) <= worst * (1 + 1e-9)
+
+
+def test_subdomain_batch_api_c5_sample(cuda):
+    """C5 shape (unit boxes, 1000 random samples, jittered lattice) on a 32-box sample."""
+    p = workloads.config5(M=64, n_sub=32, n_eval=0)
+    res = pam.fit_subdomains(p)
+    c = p.config
+    for s in (0, 17, 31):
+        a, b = p.row_off[s], p.row_off[s + 1]
+        cen = p.centres[s * 64:(s + 1) * 64]
+        W = O.shepard_features(p.points[a:b], cen, p.widths[s * 64:(s + 1) * 64])
+        o = O.fit_log(p.values[a:b], W, c.elastic.lam1, c.elastic.lam2, c.elastic.tol, c.elastic.max_iters)
+        assert np.max(np.abs(res.beta[s] - o["beta"])) <= BETA_TOL * max(1, np.abs(o["beta"]).max())
+        assert res.rounds[0].sweeps[s] == o["iterations"] or abs(res.rounds[0].sweeps[s] - o["iterations"]) <= 1
