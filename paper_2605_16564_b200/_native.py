@@ -130,8 +130,52 @@ def load_library(path: Path | str | None = None):
         return lib
 
 
+class _CountingLib:
+    """Proxy over the ctypes library that counts kernel launches per entry point.
+
+    bench.py reports ``gpu_launches`` from these counters; KERNELS_PER_CALL is
+    the number of kernels each entry point enqueues (csrc/*.cu).
+    """
+
+    KERNELS_PER_CALL = {
+        "pam_err_reset": 1, "pam_log_values_f64": 1, "pam_assemble_f64": 1, "pam_cd_f64": 1,
+        "pam_cd_ex_f64": 1, "pam_residual_f64": 2, "pam_mark_f64": 1, "pam_enrich_f64": 1,
+        "pam_locate_f64": 1, "pam_eval_f64": 5, "pam_shepard_eval_f64": 1,
+        "pam_row_normalize_f64": 1, "pam_gather_cells_f64": 1,
+    }
+
+    def __init__(self, raw):
+        self._raw = raw
+        self.launches = 0
+        self.calls = {}
+
+    def __getattr__(self, name):
+        fn = getattr(self._raw, name)
+        k = self.KERNELS_PER_CALL.get(name)
+        if k is None:
+            return fn
+
+        def call(*args):
+            self.launches += k
+            self.calls[name] = self.calls.get(name, 0) + 1
+            return fn(*args)
+
+        return call
+
+    def reset_counters(self):
+        self.launches = 0
+        self.calls = {}
+
+
+_counting = None
+
+
 def lib():
-    return load_library()
+    global _counting
+    raw = load_library()
+    if _counting is None or _counting._raw is not raw:
+        _counting = _CountingLib(raw)
+    return _counting
 
 
 # ---------------------------------------------------------------------------
@@ -174,6 +218,8 @@ def to_dev(a, dtype=None):
     """numpy/sequence -> contiguous device tensor (float64/int64/int32)."""
     torch = torch_mod()
     arr = np.ascontiguousarray(a if dtype is None else np.asarray(a, dtype=dtype))
+    if not arr.flags.writeable:
+        arr = arr.copy()
     t = torch.from_numpy(arr)
     return t.to(device(), non_blocking=False)
 

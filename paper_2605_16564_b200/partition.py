@@ -264,6 +264,9 @@ class ParallelFitReport:
     total_seconds: float
     workers: int
     max_concurrent: int
+    # B200 addition (not in the reference): per-kernel device seconds and the
+    # CD work actually done, for roofline accounting (bench.py).
+    device: dict | None = field(default=None, compare=False, repr=False)
 
 
 class _LazyChecksumMeta(dict):
@@ -333,6 +336,21 @@ def _broadcast(value, n, klass, name):
     return values
 
 
+def stage_field(data: FieldData):
+    """Keep a device copy of the (immutable) field values for repeated fits.
+
+    fit_parallel then reads the values straight from HBM (no host->device
+    copy); used by the device-resident benchmark leg.  Returns the tensor.
+    """
+    from . import _native as nat
+
+    t = data.__dict__.get("_device_values")
+    if t is None:
+        t = nat.to_dev(np.asarray(data.values, dtype=np.float64))
+        object.__setattr__(data, "_device_values", t)
+    return t
+
+
 def _batch_geometry(data: FieldData, partition: Partition):
     """Device batch (row_off host, pts dev, values dev, cell_idx dev) of all subdomains."""
     from . import _native as nat
@@ -341,7 +359,9 @@ def _batch_geometry(data: FieldData, partition: Partition):
     mesh = partition.mesh
     S = partition.n_subdomains
     dev = nat.device()
-    d_vals_all = torch.from_numpy(np.ascontiguousarray(data.values)).to(dev, non_blocking=True)
+    d_vals_all = data.__dict__.get("_device_values")
+    if d_vals_all is None:
+        d_vals_all = nat.to_dev(data.values, np.float64)
     if partition.is_cell_aligned():
         per = mesh.n_cells // S
         row_off = np.arange(S + 1, dtype=np.int64) * per
@@ -349,12 +369,18 @@ def _batch_geometry(data: FieldData, partition: Partition):
         vals = torch.empty(mesh.n_cells, dtype=torch.float64, device=dev)
         cidx = torch.empty(mesh.n_cells, dtype=torch.int64, device=dev)
         lo = np.array([b[0] for b in mesh.bounds], dtype=np.float64)
+        # keep every argument tensor alive until the launch is enqueued (the
+        # caching allocator would otherwise hand the same block out again)
+        d_counts = nat.to_dev(np.asarray(mesh.counts, dtype=np.int64))
+        d_shape = nat.to_dev(np.asarray(partition.shape, dtype=np.int32))
+        d_lo = nat.to_dev(lo)
+        d_size = nat.to_dev(np.asarray(mesh.cell_size, dtype=np.float64))
+        d_row_off = nat.to_dev(row_off)
         nat.check(nat.lib().pam_gather_cells_f64(
-            mesh.dim, nat.ptr(nat.to_dev(np.asarray(mesh.counts, dtype=np.int64))),
-            nat.ptr(nat.to_dev(np.asarray(partition.shape, dtype=np.int32))), nat.ptr(nat.to_dev(lo)),
-            nat.ptr(nat.to_dev(np.asarray(mesh.cell_size, dtype=np.float64))), nat.ptr(d_vals_all), S,
-            nat.ptr(nat.to_dev(row_off)), nat.ptr(pts), nat.ptr(vals), nat.ptr(cidx),
+            mesh.dim, nat.ptr(d_counts), nat.ptr(d_shape), nat.ptr(d_lo), nat.ptr(d_size),
+            nat.ptr(d_vals_all), S, nat.ptr(d_row_off), nat.ptr(pts), nat.ptr(vals), nat.ptr(cidx),
             nat.stream_ptr()), "pam_gather_cells_f64")
+        torch.cuda.current_stream().synchronize()  # argument tensors may be released after this
         return row_off, pts, vals, None
     # generic boxes: the reference's centroid masks (host), then one upload
     subs = partition.subdomain_fields(data)
@@ -428,6 +454,7 @@ def fit_parallel(
     rounds = [None] * n
     seconds = [0.0] * n
     dev_parts = []
+    dstats = {"kernel_seconds": {}, "cd_bytes": 0, "cd_flops": 0, "cd_launches": 0, "sweeps": 0}
     for a, b in chunks:
         sl_rows = slice(int(row_off[a]) * dim, int(row_off[b]) * dim)
         kw = {}
@@ -446,6 +473,18 @@ def fit_parallel(
             res = eng.run()
         except EngineError as exc:
             raise RuntimeError(f"fit failed on subdomain {a + exc.subdomain}: {exc.exc}") from exc.exc
+        for k, v in res.kernel_seconds.items():
+            dstats["kernel_seconds"][k] = dstats["kernel_seconds"].get(k, 0.0) + v
+        nr = n_rows[a:b]
+        for rec in res.rounds:
+            ran = rec.ran.astype(bool)
+            sw = rec.sweeps[ran].astype(np.int64)
+            nm = nr[ran] * rec.centers[ran].astype(np.int64)
+            # algorithmic CD traffic: one N x M design-matrix pass per sweep + the prologue pass
+            dstats["cd_bytes"] += int(np.sum(8 * nm * (sw + 1)))
+            dstats["cd_flops"] += int(np.sum(4 * nm * sw))  # dot + axpy, 2 FMA per entry
+            dstats["sweeps"] += int(sw.sum())
+            dstats["cd_launches"] += 1
         for s in range(b - a):
             i = a + s
             d = RbfDictionary(centers=res.centres[s], widths=res.widths[s],
@@ -461,7 +500,7 @@ def fit_parallel(
 
     report = ParallelFitReport(
         rounds=tuple(rounds), seconds=tuple(seconds), total_seconds=total, workers=workers,
-        max_concurrent=max(b - a for a, b in chunks),
+        max_concurrent=max(b - a for a, b in chunks), device=dstats,
     )
     meta = _LazyChecksumMeta(dict(metadata or {}), None if "field_checksum" in (metadata or {}) else data)
     gs = GlobalSurrogate(partition=partition, locals=tuple(locals_), metadata=meta)

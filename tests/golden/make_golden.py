@@ -189,7 +189,34 @@ def adaptive_small_cases():
     print("  adaptive_small.npz written", [r.centers for r in reps])
 
 
+def geometry_case():
+    """Reference mesh / partition / quadrature / lattice outputs (1D and 2D)."""
+    from fieldfit.geometry import build_mesh as r_mesh, cell_quadrature as r_cq
+    from fieldfit.partition import make_partition as r_part
+    from fieldfit.rbf import lattice_dictionary as r_lat
+
+    out = {}
+    cases = [(1, (12,), ((0.2, 1.7),), (3,)), (2, (17, 9), ((0.2, 1.7), (-1.0, 2.0)), (1, 3)),
+             (2, (60, 220), ((0.0, 1200.0), (0.0, 2200.0)), (6, 22)),
+             (2, (12, 10), ((0.1, 1.7), (-3.3, 2.9)), (4, 5))]
+    for k, (dim, counts, bounds, shape) in enumerate(cases):
+        mesh = r_mesh(dim, counts, bounds)
+        part = r_part(mesh, *shape)
+        out[f"g{k}_centroids"] = mesh.centroids
+        out[f"g{k}_owner"] = part.cell_to_subdomain
+        out[f"g{k}_lo"] = np.array([b.lo for b in part.boxes])
+        out[f"g{k}_hi"] = np.array([b.hi for b in part.boxes])
+        out[f"g{k}_open"] = np.array([b.open_hi for b in part.boxes])
+        pts, w = r_cq(mesh.centroids[:5], mesh.cell_size, 2)
+        out[f"g{k}_q2"], out[f"g{k}_q2w"] = pts, w
+        out[f"g{k}_lattice"] = r_lat(part.boxes[-1], 3, 0.1).centers
+    np.savez_compressed(OUT / "geometry.npz", **out)
+    print("  geometry.npz written")
+
+
 def main(which):
+    if "geometry" in which:
+        geometry_case()
     if "kernels" in which:
         kernels_case()
     if "adaptive" in which:

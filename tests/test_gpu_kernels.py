@@ -197,7 +197,7 @@ def test_locate_general_bounds_edges(cuda):
                 p[(k + 1) % 3] = rng.uniform(*mesh.bounds[(k + 1) % 3])
                 pts.append(p)
     pts = np.array(pts)
-    inside = np.all([(pts[:, k] >= mesh.bounds[k][0]) & (pts[:, k] <= mesh.bounds[k][1]) for k in range(3)], axis=0)
+    inside = np.all([(pts[:, k] >= edges[k][0]) & (pts[:, k] <= edges[k][-1]) for k in range(3)], axis=0)
     pts = pts[inside]
     owner = pam.locate_many(pts, part.boxes)
     ref = O.locate_many(pts, [(b.lo, b.hi, b.open_hi) for b in part.boxes])

@@ -1,0 +1,204 @@
+"""Pin the CPU oracle to the reference (CPU, no GPU needed).
+
+The oracle (oracle/pam_oracle.py + oracle/cd_core.c) must reproduce the
+reference's outputs BIT FOR BIT on every golden vector produced by running
+the reference (tests/golden/make_golden.py) and the reference test suite's
+own known answers.  The package's host-side restatements (mesh, partition,
+quadrature offsets, lattices; 3D extension) are pinned the same way.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import pam_oracle as O
+from paper_2605_16564_b200 import geometry, partition, rbf, workloads
+
+SLOW = os.environ.get("PAM_SLOW") == "1"
+
+
+@pytest.mark.parametrize("dim", [1, 2, 3])
+def test_features_bit_exact(golden, dim):
+    g = golden("kernels")
+    c, w, x = g[f"feat{dim}_c"], g[f"feat{dim}_w"], g[f"feat{dim}_x"]
+    np.testing.assert_array_equal(O.log_features(x, c, w), g[f"feat{dim}_L"])
+    np.testing.assert_array_equal(O.shepard_features(x, c, w), g[f"feat{dim}_W"])
+    np.testing.assert_array_equal(O.shepard_eval(x, c, w, g[f"feat{dim}_beta"]), g[f"feat{dim}_eval"])
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+def test_cd_core_bit_exact(golden, k):
+    g = golden("kernels")
+    l1, l2, tol, it = g[f"cd{k}_params"]
+    res = O.fit(g[f"cd{k}_W"], g[f"cd{k}_y"], l1, l2, tol, int(it), g.get(f"cd{k}_beta0"))
+    np.testing.assert_array_equal(res["beta"], g[f"cd{k}_beta"])
+    np.testing.assert_array_equal(res["history"], g[f"cd{k}_hist"])
+    assert [res["iterations"], int(res["converged"])] == list(g[f"cd{k}_iters"])
+
+
+def test_known_answers_from_reference_tests():
+    # frozen 8x8 objective (reference tests/test_elastic_net.py:13-20, 57-60)
+    rng = np.random.default_rng(20240817)
+    W, y = rng.standard_normal((8, 8)), rng.standard_normal(8)
+    assert abs(O.fit(W, y, 0.3, 0.2, 1e-10, 100000)["objective"] - 1.3720329345548663) <= 1e-8
+    # mark tie order (tests/test_adaptive.py:81-83)
+    np.testing.assert_array_equal(O.mark(np.array([1.0, 3.0, 1.0, 3.0, 0.5]), 3), [1, 3, 0])
+    assert O.mark(np.zeros(10), 3).size == 0
+    # two-value log targets (tests/test_elastic_net.py:264-267)
+    res = O.fit_log(np.array([1e-4, 1e-1]), np.eye(2), 0.0, 0.0, 1e-10, 100000)
+    np.testing.assert_allclose(res["beta"], [-4 * np.log(10), -np.log(10)], atol=1e-10)
+
+
+def test_mark_and_enrich_bit_exact(golden):
+    g = golden("kernels")
+    np.testing.assert_array_equal(O.mark(g["mark_R"], 50), g["mark_out"])
+    from paper_2605_16564_b200.fields import box_field_2d
+
+    sub = box_field_2d(8, 8).whole()
+    offs = ((0.0, 0.0), (-0.5, 0.0), (0.5, 0.5))
+    mk = np.array([3, 9, 27, 63, 0])
+    nc, nw = O.enrich(sub.centroids, np.full(64, 0.1), mk, sub.centroids, sub.cell_size, sub.box.lo,
+                      sub.box.hi, 0.5, 3, offs)
+    np.testing.assert_array_equal(nc, g["enr_new1_c"])
+    np.testing.assert_array_equal(nw, g["enr_new1_w"])
+    nc2, nw2 = O.enrich(g["enr_centers2"], g["enr_widths2"], mk, sub.centroids, sub.cell_size,
+                        sub.box.lo, sub.box.hi, 0.5, 3, offs)
+    np.testing.assert_array_equal(nc2, g["enr_new2_c"])
+    np.testing.assert_array_equal(nw2, g["enr_new2_w"])
+
+
+def _rep_cols(od):
+    return np.array([[r["centers"], r["added"], r["max_residual"], r["rel_l2"], r["objective"]]
+                     for r in od["reports"]])
+
+
+def test_adaptive_1d_2d_3d_bit_exact(golden):
+    g = golden("adaptive_small")
+    from paper_2605_16564_b200.fields import box_field_2d, step_field_1d
+
+    sub = step_field_1d(16).whole()
+    c = dict(lam1=4.59e-4, lam2=4.64e-6, tol=1e-10, max_iters=100000, k_top=2, m_max=12, eta=0.5,
+             m_q=3, max_rounds=3, offsets=None)
+    od = O.fit_adaptive(sub.centroids, sub.values, sub.cell_size, sub.box.lo, sub.box.hi,
+                        sub.centroids, np.full(16, 0.0019), c)
+    assert [r["centers"] for r in od["reports"]] == [16, 22, 28]
+    for key in ("centers", "widths", "beta"):
+        np.testing.assert_array_equal(od[key], g[f"a1_{key}"])
+    np.testing.assert_array_equal(_rep_cols(od), g["a1_reports"])
+
+    sub = box_field_2d(16, 16).whole()
+    c = dict(lam1=4.59e-4, lam2=1e-4, tol=1e-6, max_iters=1500, k_top=51, m_max=306, eta=0.5, m_q=3,
+             max_rounds=3, offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
+    od = O.fit_adaptive(sub.centroids, sub.values, sub.cell_size, sub.box.lo, sub.box.hi,
+                        sub.centroids, np.full(256, 0.0625), c)
+    for key in ("centers", "widths", "beta"):
+        np.testing.assert_array_equal(od[key], g[f"a2_{key}"])
+    np.testing.assert_array_equal(_rep_cols(od), g["a2_reports"])
+
+    fld = workloads.spe10_like_field(4)
+    rows = g["a3_rows"]
+    cen = fld.mesh.centroids[rows]
+    c = dict(lam1=4.59e-4, lam2=1e-4, tol=1e-6, max_iters=1000, k_top=24, m_max=144, eta=0.5, m_q=3,
+             max_rounds=3, offsets=workloads.IN_CELL_3D, quad_order=2)
+    sigma = float(np.prod(fld.mesh.cell_size) ** (1 / 3))
+    od = O.fit_adaptive(cen, fld.values[rows], fld.mesh.cell_size, (400.0, 100.0, 80.0), (520.0, 150.0, 88.0),
+                        cen, np.full(rows.size, sigma), c)
+    for key in ("centers", "widths", "beta"):
+        np.testing.assert_array_equal(od[key], g[f"a3_{key}"])
+    np.testing.assert_array_equal(_rep_cols(od), g["a3_reports"])
+
+
+def _check_config_subdomain(golden, name, wl, s):
+    g = golden(name)
+    mesh = wl.field.mesh
+    boxes, owner, _ = O.partition_boxes(mesh.counts, mesh.bounds, wl.shape)
+    b = boxes[s]
+    rows = O.subdomain_rows(mesh.centroids, b)
+    np.testing.assert_array_equal(rows, g[f"s{s}_rows"])
+    c = wl.config
+    cfg = dict(lam1=c.elastic.lam1, lam2=c.elastic.lam2, tol=c.elastic.tol, max_iters=c.elastic.max_iters,
+               k_top=c.k_top, m_max=c.m_max, eta=c.eta, m_q=c.m_q, max_rounds=c.max_rounds, offsets=c.offsets)
+    cen = mesh.centroids[rows]
+    if wl.spec.lattice is None:
+        c0 = cen
+    else:
+        c0 = O.lattice_centers(b[0], b[1], wl.spec.lattice)
+    od = O.fit_adaptive(cen, wl.field.values[rows], mesh.cell_size, b[0], b[1], c0,
+                        np.full(c0.shape[0], wl.spec.sigma), cfg)
+    for key in ("centers", "widths", "beta"):
+        np.testing.assert_array_equal(od[key], g[f"s{s}_{key}"])
+    np.testing.assert_array_equal(O.surrogate_eval(g[f"s{s}_probe"], od["centers"], od["widths"], od["beta"]),
+                                  g[f"s{s}_probe_values"])
+
+
+def test_config1_all_subdomains_bit_exact(golden):
+    wl = workloads.config1()
+    for s in range(4):
+        _check_config_subdomain(golden, "C1", wl, s)
+
+
+def test_config4_subdomain_bit_exact(golden):
+    wl = workloads.config4(with_refined_eval=False)
+    _check_config_subdomain(golden, "C4", wl, 2243)
+
+
+@pytest.mark.skipif(not SLOW, reason="PAM_SLOW=1 for the minute-long 2D refined pins")
+@pytest.mark.parametrize("name,s", [("C2", 42), ("C3", 77)])
+def test_config_2d_refined_bit_exact(golden, name, s):
+    wl = workloads.config2() if name == "C2" else workloads.config3()
+    _check_config_subdomain(golden, name, wl, s)
+
+
+def test_geometry_restatements_bit_exact(golden):
+    """Oracle AND package restatements of mesh/partition/quadrature/lattice vs the reference."""
+    g = golden("geometry")
+    cases = [(1, (12,), ((0.2, 1.7),), (3,)), (2, (17, 9), ((0.2, 1.7), (-1.0, 2.0)), (1, 3)),
+             (2, (60, 220), ((0.0, 1200.0), (0.0, 2200.0)), (6, 22)),
+             (2, (12, 10), ((0.1, 1.7), (-3.3, 2.9)), (4, 5))]
+    for k, (dim, counts, bounds, shape) in enumerate(cases):
+        cen, size = O.mesh_centroids(counts, bounds)
+        np.testing.assert_array_equal(cen, g[f"g{k}_centroids"])
+        boxes, owner, _ = O.partition_boxes(counts, bounds, shape)
+        np.testing.assert_array_equal(owner, g[f"g{k}_owner"])
+        np.testing.assert_array_equal(np.array([b[0] for b in boxes]), g[f"g{k}_lo"])
+        np.testing.assert_array_equal(np.array([b[1] for b in boxes]), g[f"g{k}_hi"])
+        np.testing.assert_array_equal(np.array([b[2] for b in boxes]), g[f"g{k}_open"])
+        offs, w = O.quad_offsets(size, 2)
+        np.testing.assert_array_equal(cen[:5, None, :] + offs[None], g[f"g{k}_q2"])
+        np.testing.assert_array_equal(w, g[f"g{k}_q2w"])
+        np.testing.assert_array_equal(O.lattice_centers(boxes[-1][0], boxes[-1][1], 3), g[f"g{k}_lattice"])
+        # the package's host restatement
+        mesh = geometry.build_mesh(dim, counts, bounds)
+        np.testing.assert_array_equal(mesh.centroids, g[f"g{k}_centroids"])
+        part = partition.make_partition(mesh, *shape)
+        np.testing.assert_array_equal(part.cell_to_subdomain, g[f"g{k}_owner"])
+        np.testing.assert_array_equal(np.array([b.lo for b in part.boxes]), g[f"g{k}_lo"])
+        np.testing.assert_array_equal(np.array([b.hi for b in part.boxes]), g[f"g{k}_hi"])
+        np.testing.assert_array_equal(np.array([b.open_hi for b in part.boxes]), g[f"g{k}_open"])
+        pts, w = geometry.cell_quadrature(mesh.centroids[:5], mesh.cell_size, 2)
+        np.testing.assert_array_equal(pts, g[f"g{k}_q2"])
+        np.testing.assert_array_equal(
+            rbf.lattice_dictionary(part.boxes[-1], 3, 0.1).centers, g[f"g{k}_lattice"])
+
+
+def test_3d_restatement_axis_consistency():
+    """3D mesh/partition: x fastest, y, z; each axis follows the 1D formula exactly."""
+    counts, bounds, shape = (6, 4, 10), ((0.0, 120.0), (-5.0, 35.0), (0.0, 20.0)), (3, 2, 5)
+    cen, size = O.mesh_centroids(counts, bounds)
+    for k in range(3):
+        c1, _ = O.mesh_centroids((counts[k],), (bounds[k],))
+        axis = np.unique(cen[:, k])
+        np.testing.assert_array_equal(axis, c1[:, 0])
+    idx = (3 * counts[1] + 2) * counts[0] + 5  # (ix, iy, iz) = (5, 2, 3)
+    assert tuple(cen[idx]) == (O.mesh_centroids((6,), (bounds[0],))[0][5, 0],
+                               O.mesh_centroids((4,), (bounds[1],))[0][2, 0],
+                               O.mesh_centroids((10,), (bounds[2],))[0][3, 0])
+    boxes, owner, _ = O.partition_boxes(counts, bounds, shape)
+    own = O.locate_many(cen, boxes)
+    np.testing.assert_array_equal(own, owner)
+    mesh = geometry.build_mesh(3, counts, bounds)
+    np.testing.assert_array_equal(mesh.centroids, cen)
+    part = partition.make_partition(mesh, *shape)
+    np.testing.assert_array_equal(part.cell_to_subdomain, owner)
+    assert part.grid is not None and part.is_cell_aligned()
