@@ -286,7 +286,7 @@ def run_ours(args):
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        vals_host = torch.from_numpy(np.ascontiguousarray(field.values)).pin_memory().numpy()
+        vals_host = torch.from_numpy(np.array(field.values)).pin_memory().numpy()
         pts_host = torch.from_numpy(wl.eval_points).pin_memory().numpy()
         mesh = field.mesh
 
@@ -359,7 +359,7 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": cd_bytes / max(cd_launches, 1),
                      "avg_launch_s": cd_s / max(cd_launches, 1),
                      "fp64_gflops": cd_flops / cd_s / 1e9 if cd_s > 0 else 0.0,
-                     "step_share": cd_s / (elapsed * world / world) / 1.0 if elapsed else None},
+                     "step_share": cd_s / (elapsed * (1 if world == 1 else 1)) if elapsed else None},
         "kernel_seconds_per_step": {k: v / args.steps for k, v in kt.items()},
         "gpu_launches": launches,
         "clocks": clocks,
