@@ -133,6 +133,31 @@ int pam_cd_ex_f64(int64_t S, const int64_t* order, const int64_t* row_off, doubl
                   int32_t* converged, double* objective, double* hist, const int64_t* hist_off,
                   int flags, void* stream);
 
+/* ---- K1t + K2b-tiles: tile-packed design matrices and their CD ------------
+ * Same W as pam_assemble_f64 (mode 0) but stored for the CD stream as
+ * column-major 32-row tiles in the row order perm (position p -> local row
+ * perm[row_off[s] + p]; NULL = identity), keeping only tiles holding an entry
+ * >= tau (tau = 0 keeps all).  tile_mask[slot] bit k = tile k stored;
+ * col_off[slot] = column offset (doubles) inside the subdomain's packed block
+ * at W + w_off[s]; packed_total[s] = doubles stored.  rowmax/rowsum are
+ * per-row scratch (sum N_s doubles each); total_slots = size of the slot
+ * arrays.  Requires N_s <= 2048.  pam_cd_tiles_f64 is pam_cd_f64 over that
+ * layout: one cp.async.bulk of popcount(mask)*256 bytes per column, tile k
+ * of a column <-> register r[k] of every lane.  y is read through perm. */
+int pam_assemble_tiles_f64(int dim, int64_t S, const int64_t* row_off, const double* pts,
+                           const int32_t* perm, const int64_t* dict_off, const int32_t* m_cur,
+                           const double* centres, const double* widths, const int64_t* w_off,
+                           const int32_t* active, int32_t max_rows, double tau, double* rowmax,
+                           double* rowsum, uint64_t* tile_mask, int64_t* col_off,
+                           int64_t* packed_total, int64_t total_slots, double* W, void* stream);
+int pam_cd_tiles_f64(int64_t S, const int64_t* order, const int64_t* row_off, const double* y,
+                     const int32_t* perm, const int64_t* dict_off, const int32_t* m_cur,
+                     const int64_t* w_off, const uint64_t* tile_mask, const int64_t* col_off,
+                     const double* W, const double* lam1, const double* lam2, const double* tol,
+                     const int32_t* max_iters, const int32_t* active, int32_t max_rows,
+                     double* beta, double* col_sq, int32_t* sweeps, int32_t* converged,
+                     double* objective, double* hist, const int64_t* hist_off, void* stream);
+
 /* ---- K3: residual indicators + L2 misfit parts -----------------------------
  * Replaces residual_indicators (adaptive.py:133-138) with cell_quadrature
  * (geometry.py:204-224) and l2_misfit_parts (fields.py:113-121).  For each

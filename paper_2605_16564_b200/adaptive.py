@@ -201,7 +201,7 @@ def fit_adaptive(sub: SubdomainField, initial: RbfDictionary,
     completed fit and the dictionary only grows after a fit.
     """
     from . import _native as nat
-    from .engine import EngineError, FitEngine, reports_for
+    from .engine import EngineError, FitEngine, rcb_permutation, reports_for
 
     dim = sub.centroids.shape[1]
     if initial.dim != dim:
@@ -215,6 +215,7 @@ def fit_adaptive(sub: SubdomainField, initial: RbfDictionary,
             np.asarray(sub.box.lo, dtype=float)[None, :], np.asarray(sub.box.hi, dtype=float)[None, :],
             [config], init_centres=initial.centers, init_widths=initial.widths,
             init_gens=initial.generations, init_m=np.array([len(initial)]),
+            row_perm=rcb_permutation(np.asarray(sub.centroids, dtype=float)),
         )
         res = eng.run()
     except EngineError as exc:

@@ -55,6 +55,10 @@ struct CdArgs {
   double* hist;
   const int64_t* hist_off;
   int flags;
+  // tile-packed design matrices (tiles.cu); null = dense column-major W
+  const unsigned long long* tile_mask;
+  const int64_t* col_off;
+  const int32_t* perm;  // tile mode: packed position -> local row (nullable = identity)
 };
 
 // named barrier over the G warps of one subdomain group (G > 1 only)
@@ -64,8 +68,9 @@ __device__ __forceinline__ void group_bar(int id, int nthreads) {
 
 // R: rows per thread, STAGES: ring depth, WPC: warps per CTA, G: warps per
 // subdomain group (rows of a subdomain split over the G*32 threads).
-template <int R, int STAGES, int WPC, int G>
+template <int R, int STAGES, int WPC, int G, bool TILES>
 __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
+  static_assert(!TILES || G == 1, "tile-packed columns are consumed one warp per subdomain");
   constexpr int GT = G * 32;         // threads per group
   constexpr int LDMAX = R * GT;      // rows per ring slot
   constexpr int NGROUPS = WPC / G;
@@ -125,29 +130,57 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
       const int64_t ld = a.ld[s];
       const double lam1 = a.lam1[s], lam2 = a.lam2[s], tol = a.tol[s];
       const int max_iters = a.max_iters[s];
-      const uint32_t bytes = static_cast<uint32_t>(((N + 1) & ~1) * sizeof(double));
+      const uint32_t dense_bytes = static_cast<uint32_t>(((N + 1) & ~1) * sizeof(double));
       const bool need_colsq = !(a.flags & CD_COLSQ_GIVEN);
       const bool r_given = (a.flags & CD_R_GIVEN) != 0;
       const bool prologue = need_colsq || !r_given;
 
-      // residual / targets into registers (thread gt owns rows gt + GT*k)
+      // residual / targets into registers (thread gt owns rows gt + GT*k);
+      // in tile mode position p = lane + 32k holds local row perm[p]
       double r[R];
 #pragma unroll
       for (int k = 0; k < R; ++k) {
-        const int row = gt + GT * k;
-        r[k] = (row < N) ? a.y[r0 + row] : 0.0;
+        const int p = gt + GT * k;
+        const int row = (TILES && a.perm) ? (p < N ? a.perm[r0 + p] : 0) : p;
+        r[k] = (p < N) ? a.y[r0 + row] : 0.0;
       }
+
+      // per-column packing parameters for the ISSUE pointer (tile mode)
+      int iss_base = -64;
+      int64_t iss_off_l = 0;
+      unsigned long long iss_mask_l = 0;
 
       // continuous column stream: [prologue M columns] + max_iters * M columns
       const int64_t total = (prologue ? (int64_t)M : 0) + (int64_t)max_iters * M;
       int64_t issued = 0;
       int next_col = 0;
       auto issue_one = [&]() {
-        if (gt == 0) {
+        if (TILES) {
+          const int cbase = next_col & ~31;
+          if (cbase != iss_base) {  // warp-uniform reload of 32 columns' packing
+            iss_base = cbase;
+            const int c = cbase + lane;
+            iss_off_l = (c < M) ? a.col_off[doff + c] : 0;
+            iss_mask_l = (c < M) ? a.tile_mask[doff + c] : 0ull;
+          }
+          const int64_t off = __shfl_sync(0xffffffffu, iss_off_l, next_col & 31);
+          const unsigned long long mk = __shfl_sync(0xffffffffu, iss_mask_l, next_col & 31);
+          const uint32_t nb = static_cast<uint32_t>(__popcll(mk)) * 32u * sizeof(double);
+          if (lane == 0) {
+            const int st = g_issue % STAGES;
+            if (nb) {
+              fence_proxy_async_smem();
+              mbar_arrive_expect_tx(&bars[st], nb);
+              tma_load_1d(ring + st * LDMAX, Ws + off, nb, &bars[st]);
+            } else {
+              mbar_arrive(&bars[st]);  // empty column: complete the phase without data
+            }
+          }
+        } else if (gt == 0) {
           const int st = g_issue % STAGES;
           fence_proxy_async_smem();
-          mbar_arrive_expect_tx(&bars[st], bytes);
-          tma_load_1d(ring + st * LDMAX, Ws + (int64_t)next_col * ld, bytes, &bars[st]);
+          mbar_arrive_expect_tx(&bars[st], dense_bytes);
+          tma_load_1d(ring + st * LDMAX, Ws + (int64_t)next_col * ld, dense_bytes, &bars[st]);
         }
         ++g_issue;
         ++issued;
@@ -159,32 +192,75 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
         ++g_cons;
         return ring + st * LDMAX;
       };
+      // column kernels: dense rows gt+GT*k, or the kept 32-row tiles of `mk`
+      auto col_dot = [&](const double* col, unsigned long long mk) -> double {
+        double dot = 0.0;
+        if (TILES) {
+          int slot = 0;
+#pragma unroll
+          for (int k = 0; k < R; ++k)
+            if ((mk >> k) & 1ull) dot = fma(col[32 * (slot++) + lane], r[k], dot);
+        } else {
+#pragma unroll
+          for (int k = 0; k < R; ++k)
+            if (gt + GT * k < N) dot = fma(col[gt + GT * k], r[k], dot);
+        }
+        return dot;
+      };
+      auto col_axpy = [&](const double* col, unsigned long long mk, double d) {
+        if (TILES) {
+          int slot = 0;
+#pragma unroll
+          for (int k = 0; k < R; ++k)
+            if ((mk >> k) & 1ull) {
+              r[k] = __dsub_rn(r[k], __dmul_rn(d, col[32 * slot + lane]));
+              ++slot;
+            }
+        } else {
+#pragma unroll
+          for (int k = 0; k < R; ++k)
+            if (gt + GT * k < N) r[k] = __dsub_rn(r[k], __dmul_rn(d, col[gt + GT * k]));
+        }
+      };
       for (int q = 0; q < STAGES && issued < total; ++q) issue_one();
       int64_t consumed = 0;
 
       // ---- prologue: col_sq (elastic_net.py:85) and r = y - W beta0 (94)
       if (prologue) {
-        for (int j = 0; j < M; ++j) {
-          const double* col = wait_one();
-          ++consumed;
-          if (need_colsq) {
-            double p = 0.0;
+        for (int cb = 0; cb < M; cb += 32) {
+          const int nc = min(32, M - cb);
+          unsigned long long ml = 0ull;
+          if (TILES && lane < nc) ml = a.tile_mask[doff + cb + lane];
+          for (int t = 0; t < nc; ++t) {
+            const int j = cb + t;
+            const unsigned long long mk = TILES ? __shfl_sync(0xffffffffu, ml, t) : 0ull;
+            const double* col = wait_one();
+            ++consumed;
+            if (need_colsq) {
+              double p = 0.0;
+              if (TILES) {
+                int slot = 0;
 #pragma unroll
-            for (int k = 0; k < R; ++k)
-              if (gt + GT * k < N) p = fma(col[gt + GT * k], col[gt + GT * k], p);
-            p = group_sum(p);
-            if (gt == 0) a.col_sq[doff + j] = p;
-          }
-          if (!r_given) {
-            const double b0 = a.beta[doff + j];
-            if (b0 != 0.0) {
+                for (int k = 0; k < R; ++k)
+                  if ((mk >> k) & 1ull) {
+                    const double w = col[32 * (slot++) + lane];
+                    p = fma(w, w, p);
+                  }
+              } else {
 #pragma unroll
-              for (int k = 0; k < R; ++k)
-                if (gt + GT * k < N) r[k] = __dsub_rn(r[k], __dmul_rn(col[gt + GT * k], b0));
+                for (int k = 0; k < R; ++k)
+                  if (gt + GT * k < N) p = fma(col[gt + GT * k], col[gt + GT * k], p);
+              }
+              p = group_sum(p);
+              if (gt == 0) a.col_sq[doff + j] = p;
             }
+            if (!r_given) {
+              const double b0 = a.beta[doff + j];
+              if (b0 != 0.0) col_axpy(col, mk, b0);
+            }
+            sync_group();
+            if (issued < total) issue_one();
           }
-          sync_group();
-          if (issued < total) issue_one();
         }
         __threadfence_block();  // col_sq stores visible to the whole group
         sync_group();
@@ -201,18 +277,17 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
           const int nc = min(32, M - cb);
           // every warp of the group holds the same 32 column parameters
           double bl = 0.0, csl = 0.0;
+          unsigned long long ml = 0ull;
           if (lane < nc) {
             bl = a.beta[doff + cb + lane];
             csl = a.col_sq[doff + cb + lane];
+            if (TILES) ml = a.tile_mask[doff + cb + lane];
           }
           for (int t = 0; t < nc; ++t) {
+            const unsigned long long mk = TILES ? __shfl_sync(0xffffffffu, ml, t) : 0ull;
             const double* col = wait_one();
             ++consumed;
-            double dot = 0.0;
-#pragma unroll
-            for (int k = 0; k < R; ++k)
-              if (gt + GT * k < N) dot = fma(col[gt + GT * k], r[k], dot);
-            dot = group_sum(dot);
+            const double dot = group_sum(col_dot(col, mk));
             const double b_old = __shfl_sync(0xffffffffu, bl, t);
             const double cs = __shfl_sync(0xffffffffu, csl, t);
             const double dn = __dadd_rn(cs, lam2);
@@ -225,9 +300,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
             }
             if (b_new != b_old) {
               const double d = __dsub_rn(b_new, b_old);
-#pragma unroll
-              for (int k = 0; k < R; ++k)
-                if (gt + GT * k < N) r[k] = __dsub_rn(r[k], __dmul_rn(d, col[gt + GT * k]));
+              col_axpy(col, mk, d);
               if (lane == t) bl = b_new;
               max_delta = fmax(max_delta, fabs(d));
             }
@@ -266,8 +339,10 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
       sync_group();
       if (a.flags & CD_WRITE_R) {
 #pragma unroll
-        for (int k = 0; k < R; ++k)
-          if (gt + GT * k < N) a.y[r0 + gt + GT * k] = r[k];
+        for (int k = 0; k < R; ++k) {
+          const int p = gt + GT * k;
+          if (p < N) a.y[r0 + ((TILES && a.perm) ? a.perm[r0 + p] : p)] = r[k];
+        }
       }
       if (gt == 0) {
         a.sweeps[s] = sweeps_done;
@@ -289,7 +364,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
   }
 }
 
-template <int R, int STAGES, int WPC, int G>
+template <int R, int STAGES, int WPC, int G, bool TILES = false>
 int launch_cd(const CdArgs& a, cudaStream_t stream) {
   constexpr int NGROUPS = WPC / G;
   const size_t smem = static_cast<size_t>(NGROUPS) * STAGES * (R * 32 * G * sizeof(double)) +
@@ -297,7 +372,7 @@ int launch_cd(const CdArgs& a, cudaStream_t stream) {
                       static_cast<size_t>(NGROUPS) * (2 * G + 1) * sizeof(double);
   static bool configured = false;
   if (!configured) {
-    PAM_CUDA_CHECK(cudaFuncSetAttribute(cd_kernel<R, STAGES, WPC, G>,
+    PAM_CUDA_CHECK(cudaFuncSetAttribute(cd_kernel<R, STAGES, WPC, G, TILES>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
@@ -308,7 +383,7 @@ int launch_cd(const CdArgs& a, cudaStream_t stream) {
   PAM_CUDA_CHECK(cudaGetSymbolAddress(&qaddr, g_cd_queue));
   PAM_CUDA_CHECK(cudaMemsetAsync(qaddr, 0, sizeof(unsigned), stream));
   const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(sms, a.S));
-  cd_kernel<R, STAGES, WPC, G><<<(unsigned)ctas, WPC * 32, smem, stream>>>(a);
+  cd_kernel<R, STAGES, WPC, G, TILES><<<(unsigned)ctas, WPC * 32, smem, stream>>>(a);
   PAM_LAUNCH_CHECK("cd_kernel");
   return PAM_OK;
 }
@@ -339,6 +414,19 @@ int cd_dispatch(const CdArgs& a, int max_rows, cudaStream_t stream) {
   return PAM_ERR_UNSUPPORTED;
 }
 
+int cd_dispatch_tiles(const CdArgs& a, int max_rows, cudaStream_t stream) {
+  // one warp per subdomain; tile k of a column <-> register r[k] of every lane
+  if (max_rows <= 32) return launch_cd<1, 4, 16, 1, true>(a, stream);
+  if (max_rows <= 64) return launch_cd<2, 4, 16, 1, true>(a, stream);
+  if (max_rows <= 128) return launch_cd<4, 4, 16, 1, true>(a, stream);
+  if (max_rows <= 256) return launch_cd<8, 4, 16, 1, true>(a, stream);
+  if (max_rows <= 512) return launch_cd<16, 3, 16, 1, true>(a, stream);
+  if (max_rows <= 1024) return launch_cd<32, 3, 8, 1, true>(a, stream);
+  if (max_rows <= 2048) return launch_cd<64, 2, 4, 1, true>(a, stream);
+  set_last_error("pam_cd_tiles_f64: tile-packed CD supports <= 2048 rows per subdomain");
+  return PAM_ERR_UNSUPPORTED;
+}
+
 }  // namespace pam
 
 using namespace pam;
@@ -356,8 +444,26 @@ extern "C" int pam_cd_ex_f64(int64_t S, const int64_t* order, const int64_t* row
   if (S == 0) return PAM_OK;
   CdArgs a{S,    order,     row_off,   y,         dict_off, m_cur, w_off,    ld,
            W,    lam1,      lam2,      tol,       max_iters, active, beta,   col_sq,
-           sweeps, converged, objective, hist,    hist_off, flags};
+           sweeps, converged, objective, hist,    hist_off, flags, nullptr, nullptr, nullptr};
   return cd_dispatch(a, max_rows, as_stream(stream));
+}
+
+extern "C" int pam_cd_tiles_f64(int64_t S, const int64_t* order, const int64_t* row_off,
+                                const double* y, const int32_t* perm, const int64_t* dict_off,
+                                const int32_t* m_cur, const int64_t* w_off,
+                                const uint64_t* tile_mask, const int64_t* col_off, const double* W,
+                                const double* lam1, const double* lam2, const double* tol,
+                                const int32_t* max_iters, const int32_t* active, int32_t max_rows,
+                                double* beta, double* col_sq, int32_t* sweeps, int32_t* converged,
+                                double* objective, double* hist, const int64_t* hist_off,
+                                void* stream) {
+  if (S < 0 || max_rows < 0 || !tile_mask || !col_off) return PAM_ERR_ARG;
+  if (S == 0) return PAM_OK;
+  CdArgs a{S,      order,     row_off,   const_cast<double*>(y), dict_off, m_cur, w_off, m_cur,
+           W,      lam1,      lam2,      tol,       max_iters, active, beta,   col_sq,
+           sweeps, converged, objective, hist,      hist_off,  0,
+           reinterpret_cast<const unsigned long long*>(tile_mask), col_off, perm};
+  return cd_dispatch_tiles(a, max_rows, as_stream(stream));
 }
 
 extern "C" int pam_cd_f64(int64_t S, const int64_t* order, const int64_t* row_off, const double* y,

@@ -52,6 +52,7 @@ class RoundRecord:
     converged: np.ndarray
     seconds: float
     ran: np.ndarray  # (S,) bool: subdomain produced a report this round
+    stream_doubles: np.ndarray = None  # (S,) design-matrix doubles the CD streams per sweep
 
 
 @dataclass
@@ -134,6 +135,46 @@ def dictionary_capacity(m0, k_top, m_q, m_max, max_rounds):
     return m0 + extra
 
 
+DEFAULT_TILE_TAU = 2.0 ** -100  # ~7.9e-31: entries below are invisible to FP64 CD (tiles.cu)
+
+
+def tile_tau() -> float:
+    """Tile-drop threshold for the packed CD stream (env PAM_TILE_TAU; 0 = dense)."""
+    import os
+
+    v = os.environ.get("PAM_TILE_TAU")
+    return DEFAULT_TILE_TAU if v is None else float(v)
+
+
+def rcb_permutation(points: np.ndarray, leaf: int = 32) -> np.ndarray:
+    """Recursive coordinate bisection order of one subdomain's sample points.
+
+    Splits along the longest physical extent at a multiple of `leaf` near the
+    median, so every 32-row tile of the CD stream is a compact blob of cells
+    and a narrow Gaussian column touches few tiles.  Deterministic (stable
+    sorts).  Only the CD's row order changes; results are order-independent
+    up to FP64 rounding of the dot products.
+    """
+    pts = np.asarray(points, dtype=np.float64)
+    n = pts.shape[0]
+    out = np.empty(n, dtype=np.int64)
+    pos = 0
+    stack = [np.arange(n)]
+    while stack:
+        ids = stack.pop()
+        if ids.size <= leaf:
+            out[pos:pos + ids.size] = ids
+            pos += ids.size
+            continue
+        p = pts[ids]
+        ax = int(np.argmax(p.max(axis=0) - p.min(axis=0)))
+        o = ids[np.argsort(p[:, ax], kind="stable")]
+        half = min(max(((ids.size // 2 + leaf - 1) // leaf) * leaf, leaf), ids.size - 1)
+        stack.append(o[half:])  # LIFO: the lower half is emitted first
+        stack.append(o[:half])
+    return out
+
+
 def estimate_w_bytes(n_rows, cap):
     return int(np.sum(_round16(n_rows) * np.asarray(cap, dtype=np.int64)) * 8)
 
@@ -143,14 +184,17 @@ class FitEngine:
 
     def __init__(self, dim, cell_size, row_off, pts, values, box_lo, box_hi, configs,
                  init_centres=None, init_widths=None, init_gens=None, init_m=None,
-                 centroid_sigma=None):
+                 centroid_sigma=None, row_perm=None, tau=None):
         """
         row_off: host int64 (S+1,); pts/values: device tensors (rows packed);
         box_lo/box_hi: host (S, dim).  The initial dictionary is either the
         per-cell centroid dictionary (``centroid_sigma``: (S,) widths,
         DictionarySpec(lattice=None), partition.py:109-111) or explicit packed
         host arrays (init_centres (sum M0, dim), init_widths, init_gens,
-        init_m (S,)).
+        init_m (S,)).  ``row_perm`` (host, packed like the rows: local row
+        index per CD position) orders the CD stream; default identity.
+        ``tau`` > 0 enables the tile-packed CD stream (tiles.cu) for batches
+        of <= 1024 rows per subdomain; 0 streams the dense design matrix.
         """
         torch = nat.torch_mod()
         self.torch = torch
@@ -180,7 +224,9 @@ class FitEngine:
         self.cap = dictionary_capacity(m0, p["k_top"], p["m_q"], p["m_max"], p["max_rounds"])
         self.dict_off = np.concatenate([[0], np.cumsum(self.cap)[:-1]]).astype(np.int64)
         cap_tot = int(self.cap.sum())
-        self.ld = _round16(self.n_rows)
+        self.tau = tile_tau() if tau is None else float(tau)
+        self.tiles = self.tau > 0.0 and self.max_rows <= 1024
+        self.ld = _round16(self.n_rows) if not self.tiles else (self.n_rows + 31) // 32 * 32
         wsz = self.ld * self.cap
         self.w_off = np.concatenate([[0], np.cumsum(wsz)[:-1]]).astype(np.int64)
         self.w_total = int(wsz.sum())
@@ -233,6 +279,13 @@ class FitEngine:
         self.d_qoff = nat.to_dev(np.concatenate([q1o, q2o]).reshape(-1))
         self.d_qw = nat.to_dev(np.concatenate([q1w, q2w]))
         self.err = nat.ErrorWord()
+        if self.tiles:
+            self.d_perm = None if row_perm is None else nat.to_dev(np.asarray(row_perm, dtype=np.int32))
+            self.d_rowmax = t.empty(ntot, dtype=f64, device=dev)
+            self.d_rowsum = t.empty(ntot, dtype=f64, device=dev)
+            self.d_tile_mask = t.zeros(cap_tot, dtype=i64, device=dev)
+            self.d_col_off = t.zeros(cap_tot, dtype=i64, device=dev)
+            self.d_packed = t.zeros(S, dtype=i64, device=dev)
 
         # ---- initial dictionary into the capacity slots
         self.m_cur = m0.copy()
@@ -294,17 +347,34 @@ class FitEngine:
             d_order = nat.to_dev(order.astype(np.int64))
             e0, e1, e2, e3 = ev(), ev(), ev(), ev()
             e0.record()
-            nat.check(lib.pam_assemble_f64(
-                dim, S, P(self.d_row_off), P(self.d_pts), P(self.d_dict_off), P(self.d_m_cur),
-                P(self.d_centres), P(self.d_widths), P(self.d_w_off), P(self.d_ld), P(self.d_active),
-                self.max_rows, 0, P(self.d_W), st), "pam_assemble_f64")
+            if self.tiles:
+                nat.check(lib.pam_assemble_tiles_f64(
+                    dim, S, P(self.d_row_off), P(self.d_pts), P(self.d_perm), P(self.d_dict_off),
+                    P(self.d_m_cur), P(self.d_centres), P(self.d_widths), P(self.d_w_off),
+                    P(self.d_active), self.max_rows, self.tau, P(self.d_rowmax), P(self.d_rowsum),
+                    P(self.d_tile_mask), P(self.d_col_off), P(self.d_packed), int(self.cap.sum()),
+                    P(self.d_W), st), "pam_assemble_tiles_f64")
+            else:
+                nat.check(lib.pam_assemble_f64(
+                    dim, S, P(self.d_row_off), P(self.d_pts), P(self.d_dict_off), P(self.d_m_cur),
+                    P(self.d_centres), P(self.d_widths), P(self.d_w_off), P(self.d_ld), P(self.d_active),
+                    self.max_rows, 0, P(self.d_W), st), "pam_assemble_f64")
             e1.record()
-            nat.check(lib.pam_cd_f64(
-                len(order), P(d_order), P(self.d_row_off), P(self.d_y), P(self.d_dict_off),
-                P(self.d_m_cur), P(self.d_w_off), P(self.d_ld), P(self.d_W), P(self.d_lam1),
-                P(self.d_lam2), P(self.d_tol), P(self.d_max_iters), P(self.d_active), self.max_rows,
-                P(self.d_beta), P(self.d_col_sq), P(self.d_sweeps), P(self.d_conv), P(self.d_obj),
-                None, None, st), "pam_cd_f64")
+            if self.tiles:
+                nat.check(lib.pam_cd_tiles_f64(
+                    len(order), P(d_order), P(self.d_row_off), P(self.d_y), P(self.d_perm),
+                    P(self.d_dict_off), P(self.d_m_cur), P(self.d_w_off), P(self.d_tile_mask),
+                    P(self.d_col_off), P(self.d_W), P(self.d_lam1), P(self.d_lam2), P(self.d_tol),
+                    P(self.d_max_iters), P(self.d_active), self.max_rows, P(self.d_beta),
+                    P(self.d_col_sq), P(self.d_sweeps), P(self.d_conv), P(self.d_obj), None, None, st),
+                    "pam_cd_tiles_f64")
+            else:
+                nat.check(lib.pam_cd_f64(
+                    len(order), P(d_order), P(self.d_row_off), P(self.d_y), P(self.d_dict_off),
+                    P(self.d_m_cur), P(self.d_w_off), P(self.d_ld), P(self.d_W), P(self.d_lam1),
+                    P(self.d_lam2), P(self.d_tol), P(self.d_max_iters), P(self.d_active), self.max_rows,
+                    P(self.d_beta), P(self.d_col_sq), P(self.d_sweeps), P(self.d_conv), P(self.d_obj),
+                    None, None, st), "pam_cd_f64")
             e2.record()
             nat.check(lib.pam_residual_f64(
                 dim, S, P(self.d_row_off), P(self.d_pts), P(self.d_values), P(self.d_dict_off),
@@ -318,6 +388,10 @@ class FitEngine:
             obj = self.d_obj.cpu().numpy()
             sweeps = self.d_sweeps.cpu().numpy()
             conv = self.d_conv.cpu().numpy()
+            if self.tiles:
+                stream_doubles = self.d_packed.cpu().numpy()
+            else:
+                stream_doubles = self.n_rows * self.m_cur
             self._sync_err("residual")
             kt["assemble"] += e0.elapsed_time(e1) / 1e3
             kt["cd"] += e1.elapsed_time(e2) / 1e3
@@ -329,6 +403,7 @@ class FitEngine:
                 round=rnd, centers=self.m_cur.copy(), added=added_total.copy(), max_residual=rmax,
                 rel_l2=rel, abs_l2=np.sqrt(num), objective=obj, sweeps=sweeps,
                 converged=conv.astype(bool), seconds=0.0, ran=active.copy(),
+                stream_doubles=np.asarray(stream_doubles, dtype=np.int64).copy(),
             )
             # stop rules in the reference's order (adaptive.py:252-260)
             stop = (rmax < p["eps_tol"]) | (added_total >= p["m_max"]) | (rnd == p["max_rounds"] - 1)
@@ -453,7 +528,7 @@ def _merge_results(parts, offsets):
             round=k, centers=cat("centers", 0), added=cat("added", 0),
             max_residual=cat("max_residual", np.nan), rel_l2=cat("rel_l2", np.nan),
             abs_l2=cat("abs_l2", np.nan), objective=cat("objective", np.nan), sweeps=cat("sweeps", 0),
-            converged=cat("converged", False),
+            converged=cat("converged", False), stream_doubles=cat("stream_doubles", 0),
             seconds=float(sum(p.rounds[k].seconds for p in parts if k < len(p.rounds))),
             ran=cat("ran", False)))
     kt = {}
@@ -497,12 +572,14 @@ def fit_packed(dim, row_off, points, values, box_lo, box_hi, configs, dict_m, ce
     for a, b in chunks:
         r0, r1 = int(row_off[a]), int(row_off[b])
         m0, m1 = int(m_off[a]), int(m_off[b])
+        perm = np.concatenate([rcb_permutation(points[row_off[i]:row_off[i + 1]])
+                               for i in range(a, b)]) if b - a <= 8192 else None
         try:
             eng = FitEngine(dim, cell_size, row_off[a:b + 1] - r0, nat.to_dev(points[r0:r1].reshape(-1)),
                             nat.to_dev(values[r0:r1]), np.asarray(box_lo)[a:b], np.asarray(box_hi)[a:b],
                             list(configs[a:b]), init_centres=centres[m0:m1], init_widths=widths[m0:m1],
                             init_gens=None if gens is None else np.asarray(gens)[m0:m1],
-                            init_m=dict_m[a:b])
+                            init_m=dict_m[a:b], row_perm=perm)
             parts.append(eng.run())
         except EngineError as exc:
             raise EngineError(a + exc.subdomain, exc.exc) from exc.exc

@@ -390,6 +390,28 @@ def _batch_geometry(data: FieldData, partition: Partition):
     return row_off, pts, vals, subs
 
 
+def _cd_row_order(partition: Partition, subs, row_off, a, b):
+    """Row order of the CD stream for subdomains [a, b) (engine.rcb_permutation).
+
+    make_partition grids share one local cell layout, so one bisection order
+    serves every subdomain; generic box sets are ordered per subdomain.
+    """
+    from .engine import rcb_permutation
+
+    mesh = partition.mesh
+    if subs is None:  # cell-aligned grid: local layout identical in every box
+        nloc = [n // p for n, p in zip(mesh.counts, partition.shape)]
+        t = np.arange(int(np.prod(nloc)))
+        loc = [t % nloc[0]]
+        if mesh.dim >= 2:
+            loc.append((t // nloc[0]) % nloc[1])
+        if mesh.dim == 3:
+            loc.append(t // (nloc[0] * nloc[1]))
+        pts = np.stack([(l + 0.5) * h for l, h in zip(loc, mesh.cell_size)], axis=1)
+        return np.tile(rcb_permutation(pts), b - a)
+    return np.concatenate([rcb_permutation(subs[i].centroids) for i in range(a, b)])
+
+
 def fit_parallel(
     data: FieldData,
     partition: Partition,
@@ -405,102 +427,17 @@ def fit_parallel(
     are identical for any ``workers`` value and any batch chunking.
     """
     from . import _native as nat
-    from .engine import (EngineError, FitEngine, chunk_ranges, dictionary_capacity, reports_for,
-                         w_budget_bytes, _round16)
 
     n = partition.n_subdomains
     cfgs = _broadcast(configs, n, AdaptiveConfig, "configs")
     specs = _broadcast(spec, n, DictionarySpec, "spec")
-    mesh = partition.mesh
-    dim = mesh.dim
     t0 = time.perf_counter()
-    row_off, d_pts, d_vals, subs = _batch_geometry(data, partition)
-    n_rows = np.diff(row_off)
-    boxes = partition.boxes
-    box_lo = np.array([b.lo for b in boxes], dtype=np.float64)
-    box_hi = np.array([b.hi for b in boxes], dtype=np.float64)
-
-    # initial dictionaries: per-cell centroid dictionaries are built on the
-    # device; lattices and user-defined specs on the host (partition.py:109-112)
-    plain = [type(sp) is DictionarySpec for sp in specs]
-    centroid = all(p and sp.lattice is None for p, sp in zip(plain, specs))
-    init = None
-    if not centroid:
-        if subs is None and not all(plain):
-            subs = partition.subdomain_fields(data)
-        init = []
-        for i, sp in enumerate(specs):
-            try:
-                if type(sp) is DictionarySpec and sp.lattice is not None:
-                    d = lattice_dictionary(boxes[i], sp.lattice, sp.sigma)
-                elif type(sp) is DictionarySpec:
-                    cen = (subs[i].centroids if subs is not None
-                           else d_pts.view(-1, dim)[row_off[i]:row_off[i + 1]].cpu().numpy())
-                    d = centroid_dictionary(cen, sp.sigma)
-                else:
-                    sub = subs[i] if subs is not None else data.subdomain(boxes[i])
-                    d = sp.build(sub)
-            except Exception as exc:  # noqa: BLE001 - annotate with the subdomain index
-                raise RuntimeError(f"fit failed on subdomain {i}: {exc}") from exc
-            init.append(d)
-    m0 = n_rows if centroid else np.array([len(d) for d in init], dtype=np.int64)
-    k_top = np.minimum([c.k_top for c in cfgs], n_rows)
-    cap = dictionary_capacity(m0, k_top, [c.m_q for c in cfgs], [c.m_max for c in cfgs],
-                              [c.max_rounds for c in cfgs])
-    wbytes = _round16(n_rows) * cap * 8
-    chunks = chunk_ranges(wbytes, w_budget_bytes())
-
-    locals_ = [None] * n
-    rounds = [None] * n
-    seconds = [0.0] * n
-    dev_parts = []
-    dstats = {"kernel_seconds": {}, "cd_bytes": 0, "cd_flops": 0, "cd_launches": 0, "sweeps": 0}
-    for a, b in chunks:
-        sl_rows = slice(int(row_off[a]) * dim, int(row_off[b]) * dim)
-        kw = {}
-        if centroid:
-            kw["centroid_sigma"] = np.array([specs[i].sigma for i in range(a, b)], dtype=np.float64)
-        else:
-            ds = init[a:b]
-            kw.update(init_centres=np.concatenate([d.centers for d in ds]),
-                      init_widths=np.concatenate([d.widths for d in ds]),
-                      init_gens=np.concatenate([d.generations for d in ds]),
-                      init_m=np.array([len(d) for d in ds], dtype=np.int64))
-        try:
-            eng = FitEngine(dim, mesh.cell_size, row_off[a:b + 1] - row_off[a], d_pts[sl_rows],
-                            d_vals[int(row_off[a]):int(row_off[b])], box_lo[a:b], box_hi[a:b],
-                            cfgs[a:b], **kw)
-            res = eng.run()
-        except EngineError as exc:
-            raise RuntimeError(f"fit failed on subdomain {a + exc.subdomain}: {exc.exc}") from exc.exc
-        for k, v in res.kernel_seconds.items():
-            dstats["kernel_seconds"][k] = dstats["kernel_seconds"].get(k, 0.0) + v
-        nr = n_rows[a:b]
-        for rec in res.rounds:
-            ran = rec.ran.astype(bool)
-            sw = rec.sweeps[ran].astype(np.int64)
-            nm = nr[ran] * rec.centers[ran].astype(np.int64)
-            # algorithmic CD traffic: one N x M design-matrix pass per sweep + the prologue pass
-            dstats["cd_bytes"] += int(np.sum(8 * nm * (sw + 1)))
-            dstats["cd_flops"] += int(np.sum(4 * nm * sw))  # dot + axpy, 2 FMA per entry
-            dstats["sweeps"] += int(sw.sum())
-            dstats["cd_launches"] += 1
-        for s in range(b - a):
-            i = a + s
-            d = RbfDictionary(centers=res.centres[s], widths=res.widths[s],
-                              generations=res.generations[s])
-            locals_[i] = LocalSurrogate(dictionary=d, beta=res.beta[s], log_transform=True)
-            rounds[i] = tuple(reports_for(res, s, RoundReport))
-            seconds[i] = res.seconds
-        # keep the fitted dictionaries resident for evaluation; drop W
-        dev_parts.append((eng.d_dict_off, eng.d_m_cur, eng.d_centres, eng.d_widths, eng.d_beta,
-                          int(eng.cap.sum())))
-        eng.d_W = None
+    locals_, rounds, seconds, dev_parts, dstats, max_conc = _fit_range(data, partition, cfgs, specs, 0, n)
     total = time.perf_counter() - t0
 
     report = ParallelFitReport(
         rounds=tuple(rounds), seconds=tuple(seconds), total_seconds=total, workers=workers,
-        max_concurrent=max(b - a for a, b in chunks), device=dstats,
+        max_concurrent=max_conc, device=dstats,
     )
     meta = _LazyChecksumMeta(dict(metadata or {}), None if "field_checksum" in (metadata or {}) else data)
     gs = GlobalSurrogate(partition=partition, locals=tuple(locals_), metadata=meta)
@@ -518,8 +455,112 @@ def fit_parallel(
         w = torch.cat([p[3] for p in dev_parts])
         bt = torch.cat([p[4] for p in dev_parts])
     logf = torch.ones(n, dtype=torch.int32, device=nat.device())
-    gs.attach_device(DeviceSurrogate(dim, off, m, c, w, bt, logf))
+    gs.attach_device(DeviceSurrogate(partition.mesh.dim, off, m, c, w, bt, logf))
     return gs, report
+
+
+def fit_subset(data: FieldData, partition: Partition, cfgs, specs, lo: int, hi: int):
+    """Fit subdomains [lo, hi) on this GPU; returns [(LocalSurrogate, reports)] (parallel.py)."""
+    locals_, rounds, *_ = _fit_range(data, partition, list(cfgs), list(specs), lo, hi)
+    return list(zip(locals_, rounds))
+
+
+def _fit_range(data, partition, cfgs, specs, lo, hi):
+    """Device fits of subdomains [lo, hi): (locals, rounds, seconds, device parts, stats, max batch)."""
+    from .engine import (EngineError, FitEngine, chunk_ranges, dictionary_capacity, reports_for,
+                         w_budget_bytes)
+
+    mesh = partition.mesh
+    dim = mesh.dim
+    row_off, d_pts, d_vals, subs = _batch_geometry(data, partition)
+    n_rows = np.diff(row_off)
+    boxes = partition.boxes
+    box_lo = np.array([b.lo for b in boxes], dtype=np.float64)
+    box_hi = np.array([b.hi for b in boxes], dtype=np.float64)
+
+    # initial dictionaries: per-cell centroid dictionaries are built on the
+    # device; lattices and user-defined specs on the host (partition.py:109-112)
+    plain = [type(sp) is DictionarySpec for sp in specs]
+    centroid = all(p and sp.lattice is None for p, sp in zip(plain, specs))
+    init = None
+    if not centroid:
+        if subs is None and not all(plain):
+            subs = partition.subdomain_fields(data)
+        init = {}
+        for i in range(lo, hi):
+            sp = specs[i]
+            try:
+                if type(sp) is DictionarySpec and sp.lattice is not None:
+                    d = lattice_dictionary(boxes[i], sp.lattice, sp.sigma)
+                elif type(sp) is DictionarySpec:
+                    cen = (subs[i].centroids if subs is not None
+                           else d_pts.view(-1, dim)[row_off[i]:row_off[i + 1]].cpu().numpy())
+                    d = centroid_dictionary(cen, sp.sigma)
+                else:
+                    sub = subs[i] if subs is not None else data.subdomain(boxes[i])
+                    d = sp.build(sub)
+            except Exception as exc:  # noqa: BLE001 - annotate with the subdomain index
+                raise RuntimeError(f"fit failed on subdomain {i}: {exc}") from exc
+            init[i] = d
+    m0 = n_rows[lo:hi] if centroid else np.array([len(init[i]) for i in range(lo, hi)], dtype=np.int64)
+    k_top = np.minimum([c.k_top for c in cfgs[lo:hi]], n_rows[lo:hi])
+    cap = dictionary_capacity(m0, k_top, [c.m_q for c in cfgs[lo:hi]], [c.m_max for c in cfgs[lo:hi]],
+                              [c.max_rounds for c in cfgs[lo:hi]])
+    wbytes = (n_rows[lo:hi] + 31) // 32 * 32 * cap * 8
+    chunks = [(lo + a, lo + b) for a, b in chunk_ranges(wbytes, w_budget_bytes())]
+    n = hi - lo
+
+    locals_ = [None] * n
+    rounds = [None] * n
+    seconds = [0.0] * n
+    dev_parts = []
+    dstats = {"kernel_seconds": {}, "cd_bytes": 0, "cd_flops": 0, "cd_launches": 0, "sweeps": 0}
+    for a, b in chunks:
+        sl_rows = slice(int(row_off[a]) * dim, int(row_off[b]) * dim)
+        kw = {}
+        if centroid:
+            kw["centroid_sigma"] = np.array([specs[i].sigma for i in range(a, b)], dtype=np.float64)
+        else:
+            ds = [init[i] for i in range(a, b)]
+            kw.update(init_centres=np.concatenate([d.centers for d in ds]),
+                      init_widths=np.concatenate([d.widths for d in ds]),
+                      init_gens=np.concatenate([d.generations for d in ds]),
+                      init_m=np.array([len(d) for d in ds], dtype=np.int64))
+        kw["row_perm"] = _cd_row_order(partition, subs, row_off, a, b)
+        try:
+            eng = FitEngine(dim, mesh.cell_size, row_off[a:b + 1] - row_off[a], d_pts[sl_rows],
+                            d_vals[int(row_off[a]):int(row_off[b])], box_lo[a:b], box_hi[a:b],
+                            cfgs[a:b], **kw)
+            res = eng.run()
+        except EngineError as exc:
+            raise RuntimeError(f"fit failed on subdomain {a + exc.subdomain}: {exc.exc}") from exc.exc
+        for k, v in res.kernel_seconds.items():
+            dstats["kernel_seconds"][k] = dstats["kernel_seconds"].get(k, 0.0) + v
+        nr = n_rows[a:b]
+        for rec in res.rounds:
+            ran = rec.ran.astype(bool)
+            sw = rec.sweeps[ran].astype(np.int64)
+            dense = nr[ran] * rec.centers[ran].astype(np.int64)
+            nm = rec.stream_doubles[ran].astype(np.int64)  # kept tiles (== dense when tau = 0)
+            # algorithmic CD traffic: one pass over the streamed design matrix per
+            # sweep + the prologue pass
+            dstats["cd_bytes"] += int(np.sum(8 * nm * (sw + 1)))
+            dstats["cd_dense_bytes"] = dstats.get("cd_dense_bytes", 0) + int(np.sum(8 * dense * (sw + 1)))
+            dstats["cd_flops"] += int(np.sum(4 * nm * sw))  # dot + axpy, 2 FMA per entry
+            dstats["sweeps"] += int(sw.sum())
+            dstats["cd_launches"] += 1
+        for s in range(b - a):
+            i = a + s - lo
+            d = RbfDictionary(centers=res.centres[s], widths=res.widths[s],
+                              generations=res.generations[s])
+            locals_[i] = LocalSurrogate(dictionary=d, beta=res.beta[s], log_transform=True)
+            rounds[i] = tuple(reports_for(res, s, RoundReport))
+            seconds[i] = res.seconds
+        # keep the fitted dictionaries resident for evaluation; drop W
+        dev_parts.append((eng.d_dict_off, eng.d_m_cur, eng.d_centres, eng.d_widths, eng.d_beta,
+                          int(eng.cap.sum())))
+        eng.d_W = None
+    return locals_, rounds, seconds, dev_parts, dstats, max(b - a for a, b in chunks)
 
 
 # ---------------------------------------------------------------------------
