@@ -212,6 +212,28 @@ def test_fit_parallel_deterministic_and_chunk_independent(cuda, monkeypatch):
     assert pam.dumps(s1) == pam.dumps(s4)
 
 
+@pytest.mark.parametrize("cells", [(16, 16), (40, 40)])
+def test_tile_packed_stream_matches_dense(cuda, monkeypatch, cells):
+    """Tile-dropping (tau = 2^-100) vs exact dense streaming: same decisions, beta ~1e-12."""
+    field = pam.box_field_2d(*cells)
+    part = pam.make_partition(field.mesh, 2, 2)
+    cfg = pam.AdaptiveConfig(k_top=cells[0], m_max=6 * cells[0], m_q=3, max_rounds=3, elastic=EN_2D,
+                             offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
+    spec = pam.DictionarySpec(sigma=0.5 / cells[0])
+    monkeypatch.setenv("PAM_TILE_TAU", "0")
+    dense, rd = pam.fit_parallel(field, part, cfg, spec)
+    monkeypatch.setenv("PAM_TILE_TAU", str(2.0 ** -100))
+    tiled, rt = pam.fit_parallel(field, part, cfg, spec)
+    assert rt.device["cd_bytes"] < rd.device["cd_bytes"]  # tiles were actually dropped
+    for a, b in zip(dense.locals, tiled.locals):
+        np.testing.assert_array_equal(a.dictionary.centers, b.dictionary.centers)
+        assert np.max(np.abs(a.beta - b.beta)) <= 1e-10 * max(1, np.abs(a.beta).max())
+    for ra, rb in zip(rd.rounds, rt.rounds):
+        assert [r.centers for r in ra] == [r.centers for r in rb]
+        for x, y in zip(ra, rb):
+            assert abs(x.rel_l2 - y.rel_l2) <= 1e-10 * x.rel_l2
+
+
 class _BrokenSpec(pam.DictionarySpec):
     def build(self, sub):
         raise RuntimeError("boom")
