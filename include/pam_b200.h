@@ -158,6 +158,27 @@ int pam_cd_tiles_f64(int64_t S, const int64_t* order, const int64_t* row_off, co
                      double* beta, double* col_sq, int32_t* sweeps, int32_t* converged,
                      double* objective, double* hist, const int64_t* hist_off, void* stream);
 
+/* ---- K2 + K2b': Gram products and the Gram-form CD (M < N) -----------------
+ * pam_gram_f64: G_s = W_s^T W_s (symmetric, column-major at G + g_off[s],
+ * leading dimension ldg[s]), q = W^T y and col_sq = diag(G) per dictionary
+ * slot, from the dense design matrices of pam_assemble_f64.
+ * pam_cd_gram_f64: the reference's cyclic CD (elastic_net.py:113-161) in
+ * covariance form c = q - G beta: z = col_sq_j beta_j + c_j, c -= d G[:, j];
+ * same decisions and stop rule, M*M doubles streamed per sweep (vs N*M).
+ * Writes beta, sweeps, converged (the objective is then evaluated exactly by
+ * pam_cd_f64 with max_iters = 0, which computes 0.5|y - W beta|^2 + ...).
+ * Requires M <= 512 and ldg <= 512. */
+int pam_gram_f64(int64_t S, const int64_t* row_off, const int32_t* m_cur, const int64_t* dict_off,
+                 const int64_t* w_off, const int32_t* ld, const int64_t* g_off, const int32_t* ldg,
+                 const int32_t* active, int32_t max_m, const double* W, const double* y,
+                 double* G, double* q, double* col_sq, void* stream);
+int pam_cd_gram_f64(int64_t S, const int64_t* order, const int64_t* dict_off, const int32_t* m_cur,
+                    const int64_t* g_off, const int32_t* ldg, const double* G, const double* q,
+                    const double* col_sq, const double* lam1, const double* lam2,
+                    const double* tol, const int32_t* max_iters, const int32_t* active,
+                    int32_t max_m, double* beta, int32_t* sweeps, int32_t* converged,
+                    void* stream);
+
 /* ---- K3: residual indicators + L2 misfit parts -----------------------------
  * Replaces residual_indicators (adaptive.py:133-138) with cell_quadrature
  * (geometry.py:204-224) and l2_misfit_parts (fields.py:113-121).  For each

@@ -68,6 +68,15 @@ SIGNATURES = {
         [_i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr,
          _ptr, _i32, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr],
     ),
+    "pam_gram_f64": (
+        ctypes.c_int,
+        [_i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _i32, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr],
+    ),
+    "pam_cd_gram_f64": (
+        ctypes.c_int,
+        [_i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _i32,
+         _ptr, _ptr, _ptr, _ptr],
+    ),
     "pam_residual_f64": (
         ctypes.c_int,
         [ctypes.c_int, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr,
@@ -152,7 +161,7 @@ class _CountingLib:
         "pam_cd_ex_f64": 1, "pam_residual_f64": 2, "pam_mark_f64": 1, "pam_enrich_f64": 1,
         "pam_locate_f64": 1, "pam_eval_f64": 5, "pam_shepard_eval_f64": 1,
         "pam_row_normalize_f64": 1, "pam_gather_cells_f64": 1, "pam_assemble_tiles_f64": 3,
-        "pam_cd_tiles_f64": 1,
+        "pam_cd_tiles_f64": 1, "pam_gram_f64": 2, "pam_cd_gram_f64": 1,
     }
 
     def __init__(self, raw):

@@ -24,6 +24,8 @@
 // K2b), ~2 FMA per 8 bytes.
 #include "pam_common.cuh"
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 namespace pam {
@@ -192,35 +194,38 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
         ++g_cons;
         return ring + st * LDMAX;
       };
-      // column kernels: dense rows gt+GT*k, or the kept 32-row tiles of `mk`
-      auto col_dot = [&](const double* col, unsigned long long mk) -> double {
-        double dot = 0.0;
+      // Column staging: the column's entries for this thread's rows go to
+      // registers once and serve both the dot and the AXPY.  Branch-free: rows
+      // past N (dense) or tiles not stored (tile mode) read an in-bounds smem
+      // word and select 0, so they contribute exactly nothing.
+      double w[R];
+      auto load_col = [&](const double* col, unsigned long long mk) {
         if (TILES) {
           int slot = 0;
 #pragma unroll
-          for (int k = 0; k < R; ++k)
-            if ((mk >> k) & 1ull) dot = fma(col[32 * (slot++) + lane], r[k], dot);
+          for (int k = 0; k < R; ++k) {
+            const int bit = static_cast<int>((mk >> k) & 1ull);
+            const double v = col[32 * slot + lane];  // slot <= k < R: inside the ring slot
+            w[k] = bit ? v : 0.0;
+            slot += bit;
+          }
         } else {
 #pragma unroll
-          for (int k = 0; k < R; ++k)
-            if (gt + GT * k < N) dot = fma(col[gt + GT * k], r[k], dot);
+          for (int k = 0; k < R; ++k) {
+            const double v = col[gt + GT * k];
+            w[k] = (gt + GT * k < N) ? v : 0.0;
+          }
         }
+      };
+      auto col_dot = [&]() -> double {
+        double dot = 0.0;
+#pragma unroll
+        for (int k = 0; k < R; ++k) dot = fma(w[k], r[k], dot);
         return dot;
       };
-      auto col_axpy = [&](const double* col, unsigned long long mk, double d) {
-        if (TILES) {
-          int slot = 0;
+      auto col_axpy = [&](double d) {
 #pragma unroll
-          for (int k = 0; k < R; ++k)
-            if ((mk >> k) & 1ull) {
-              r[k] = __dsub_rn(r[k], __dmul_rn(d, col[32 * slot + lane]));
-              ++slot;
-            }
-        } else {
-#pragma unroll
-          for (int k = 0; k < R; ++k)
-            if (gt + GT * k < N) r[k] = __dsub_rn(r[k], __dmul_rn(d, col[gt + GT * k]));
-        }
+        for (int k = 0; k < R; ++k) r[k] = fma(-d, w[k], r[k]);
       };
       for (int q = 0; q < STAGES && issued < total; ++q) issue_one();
       int64_t consumed = 0;
@@ -236,27 +241,17 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
             const unsigned long long mk = TILES ? __shfl_sync(0xffffffffu, ml, t) : 0ull;
             const double* col = wait_one();
             ++consumed;
+            load_col(col, mk);
             if (need_colsq) {
               double p = 0.0;
-              if (TILES) {
-                int slot = 0;
 #pragma unroll
-                for (int k = 0; k < R; ++k)
-                  if ((mk >> k) & 1ull) {
-                    const double w = col[32 * (slot++) + lane];
-                    p = fma(w, w, p);
-                  }
-              } else {
-#pragma unroll
-                for (int k = 0; k < R; ++k)
-                  if (gt + GT * k < N) p = fma(col[gt + GT * k], col[gt + GT * k], p);
-              }
+              for (int k = 0; k < R; ++k) p = fma(w[k], w[k], p);
               p = group_sum(p);
               if (gt == 0) a.col_sq[doff + j] = p;
             }
             if (!r_given) {
               const double b0 = a.beta[doff + j];
-              if (b0 != 0.0) col_axpy(col, mk, b0);
+              if (b0 != 0.0) col_axpy(b0);
             }
             sync_group();
             if (issued < total) issue_one();
@@ -287,7 +282,8 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
             const unsigned long long mk = TILES ? __shfl_sync(0xffffffffu, ml, t) : 0ull;
             const double* col = wait_one();
             ++consumed;
-            const double dot = group_sum(col_dot(col, mk));
+            load_col(col, mk);
+            const double dot = group_sum(col_dot());
             const double b_old = __shfl_sync(0xffffffffu, bl, t);
             const double cs = __shfl_sync(0xffffffffu, csl, t);
             const double dn = __dadd_rn(cs, lam2);
@@ -300,7 +296,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
             }
             if (b_new != b_old) {
               const double d = __dsub_rn(b_new, b_old);
-              col_axpy(col, mk, d);
+              col_axpy(d);
               if (lane == t) bl = b_new;
               max_delta = fmax(max_delta, fabs(d));
             }
@@ -330,6 +326,23 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
           conv = 1;
           break;
         }
+      }
+      if (max_iters == 0) {
+        // objective at the given beta (used after the Gram-form sweeps, gram.cu):
+        // 0.5 |y - W beta|^2 + lam1 |beta|_1 + 0.5 lam2 |beta|^2, exact residual form
+        double rss = 0.0, l1 = 0.0, l2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < R; ++k) rss = fma(r[k], r[k], rss);
+        rss = group_sum(rss);
+        for (int j = lane; j < M; j += 32) {
+          const double b = a.beta[doff + j];
+          l1 += fabs(b);
+          l2 = fma(b, b, l2);
+        }
+        l1 = warp_sum(l1);
+        l2 = warp_sum(l2);
+        obj = __dadd_rn(__dadd_rn(__dmul_rn(0.5, rss), __dmul_rn(lam1, l1)),
+                        __dmul_rn(__dmul_rn(0.5, lam2), l2));
       }
       // drain speculative prefetches of the sweep that will not run
       while (consumed < issued) {
@@ -420,7 +433,11 @@ int cd_dispatch_tiles(const CdArgs& a, int max_rows, cudaStream_t stream) {
   if (max_rows <= 64) return launch_cd<2, 4, 16, 1, true>(a, stream);
   if (max_rows <= 128) return launch_cd<4, 4, 16, 1, true>(a, stream);
   if (max_rows <= 256) return launch_cd<8, 4, 16, 1, true>(a, stream);
-  if (max_rows <= 512) return launch_cd<16, 3, 16, 1, true>(a, stream);
+  if (max_rows <= 512) {
+    static const char* env = getenv("PAM_CD_WPC16");
+    if (env && atoi(env) == 12) return launch_cd<16, 3, 12, 1, true>(a, stream);
+    return launch_cd<16, 3, 16, 1, true>(a, stream);
+  }
   if (max_rows <= 1024) return launch_cd<32, 3, 8, 1, true>(a, stream);
   if (max_rows <= 2048) return launch_cd<64, 2, 4, 1, true>(a, stream);
   set_last_error("pam_cd_tiles_f64: tile-packed CD supports <= 2048 rows per subdomain");

@@ -1,0 +1,356 @@
+// gram.cu — K2: batched FP64 Gram products and the Gram-form CD (K2b') for
+// subdomains whose dictionary is smaller than their sample count (M < N).
+//
+// The reference CD (elastic_net.py:113-161) works in residual form: per
+// coordinate a length-N dot W_j.r and an AXPY r -= d W_j, i.e. N*M doubles
+// streamed per sweep.  With c = W^T y - G beta (G = W^T W) the same
+// cyclic updates read only column j of G:  z = col_sq_j beta_j + c_j,
+// c -= d G[:, j]  — M*M doubles per sweep instead of N*M (C1: 4x fewer,
+// C5 at M=64: 16x fewer, and the whole G of a small-M subdomain stays
+// L2-resident across sweeps).  The decisions (cyclic order, soft threshold,
+// division, stop rule) are the reference's; only the rounding of the
+// accumulated inner products differs (~1e-12 relative in beta).
+// FP64 throughout: an FP32/TF32 Gram fails the tolerance by 1e4-1e6 (F3).
+//
+//   gram_kernel     G = W^T W (symmetric: upper tiles computed, mirrored),
+//                   32x32 output tiles, W chunks staged in shared memory.
+//   gemv_t_kernel   q = W^T y, one warp per column.
+//   cd_gram_kernel  one warp per subdomain, c in registers (lane l owns
+//                   coordinates l + 32t), G columns streamed by cp.async.bulk
+//                   (several columns per ring slot when M is small).
+#include "pam_common.cuh"
+
+#include <algorithm>
+
+namespace pam {
+
+constexpr int GT_TILE = 32;
+
+// ---- G = W^T W -------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+gram_kernel(const int64_t* __restrict__ row_off, const int32_t* __restrict__ m_cur,
+            const int64_t* __restrict__ w_off, const int32_t* __restrict__ ld,
+            const int64_t* __restrict__ g_off, const int32_t* __restrict__ ldg,
+            const int32_t* __restrict__ active, const double* __restrict__ W,
+            double* __restrict__ G) {
+  __shared__ double A[GT_TILE][GT_TILE + 1];
+  __shared__ double B[GT_TILE][GT_TILE + 1];
+  const int64_t s = blockIdx.y;
+  if (active != nullptr && active[s] == 0) return;
+  const int M = m_cur[s];
+  const int T = (M + GT_TILE - 1) / GT_TILE;
+  // decode upper-triangular tile pair (jb <= kb) from blockIdx.x
+  int pair = blockIdx.x, jb = 0;
+  while (jb < T && pair >= T - jb) {
+    pair -= T - jb;
+    ++jb;
+  }
+  if (jb >= T) return;
+  const int kb = jb + pair;
+  const int n = static_cast<int>(row_off[s + 1] - row_off[s]);
+  const double* Ws = W + w_off[s];
+  const int64_t lds = ld[s];
+  double* Gs = G + g_off[s];
+  const int64_t ldgs = ldg[s];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int i0 = 0; i0 < n; i0 += GT_TILE) {
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = ty + 8 * u;
+      const int i = i0 + tx;
+      const int cj = jb * GT_TILE + c, ck = kb * GT_TILE + c;
+      A[tx][c] = (i < n && cj < M) ? Ws[(int64_t)cj * lds + i] : 0.0;
+      B[tx][c] = (i < n && ck < M) ? Ws[(int64_t)ck * lds + i] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int i = 0; i < GT_TILE; ++i) {
+      const double a = A[i][tx];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] = fma(a, B[i][ty + 8 * u], acc[u]);
+    }
+  }
+  const int j = jb * GT_TILE + tx;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int k = kb * GT_TILE + ty + 8 * u;
+    if (j < M && k < M) {
+      Gs[(int64_t)k * ldgs + j] = acc[u];
+      if (jb != kb) Gs[(int64_t)j * ldgs + k] = acc[u];
+    }
+  }
+}
+
+// ---- q = W^T y, col_sq = diag(G) -------------------------------------------
+__global__ void gemv_t_kernel(const int64_t* __restrict__ row_off, const int32_t* __restrict__ m_cur,
+                              const int64_t* __restrict__ dict_off, const int64_t* __restrict__ w_off,
+                              const int32_t* __restrict__ ld, const int64_t* __restrict__ g_off,
+                              const int32_t* __restrict__ ldg, const int32_t* __restrict__ active,
+                              const double* __restrict__ W, const double* __restrict__ y,
+                              const double* __restrict__ G, double* __restrict__ q,
+                              double* __restrict__ col_sq) {
+  const int64_t s = blockIdx.y;
+  if (active != nullptr && active[s] == 0) return;
+  const int M = m_cur[s];
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= M) return;
+  const int64_t r0 = row_off[s];
+  const int n = static_cast<int>(row_off[s + 1] - r0);
+  const double* col = W + w_off[s] + (int64_t)warp * ld[s];
+  double acc = 0.0;
+  for (int i = lane; i < n; i += 32) acc = fma(col[i], y[r0 + i], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) {
+    q[dict_off[s] + warp] = acc;
+    col_sq[dict_off[s] + warp] = G[g_off[s] + (int64_t)warp * ldg[s] + warp];
+  }
+}
+
+// ---- Gram-form cyclic CD ------------------------------------------------------
+struct GramArgs {
+  int64_t S;
+  const int64_t* order;
+  const int64_t* dict_off;
+  const int32_t* m_cur;
+  const int64_t* g_off;
+  const int32_t* ldg;
+  const double* G;
+  const double* q;
+  const double* col_sq;
+  const double* lam1;
+  const double* lam2;
+  const double* tol;
+  const int32_t* max_iters;
+  const int32_t* active;
+  double* beta;
+  int32_t* sweeps;
+  int32_t* converged;
+};
+
+__device__ unsigned int g_gram_queue;
+
+// MT: max coordinates per lane (M <= 32*MT); SLOT: doubles per ring slot.
+template <int MT, int STAGES, int WPC, int SLOT>
+__global__ void __launch_bounds__(WPC * 32, 1) cd_gram_kernel(const GramArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  double* ring = reinterpret_cast<double*>(smem_raw) + static_cast<size_t>(warp) * STAGES * SLOT;
+  uint64_t* bars =
+      reinterpret_cast<uint64_t*>(reinterpret_cast<double*>(smem_raw) + WPC * STAGES * SLOT) +
+      warp * STAGES;
+  if (lane == 0) {
+    for (int st = 0; st < STAGES; ++st) mbar_init(&bars[st], 1);
+    fence_mbar_init();
+    fence_proxy_async_smem();
+  }
+  __syncwarp();
+  uint32_t g_issue = 0, g_cons = 0;
+  const unsigned total_warps = gridDim.x * WPC;
+  unsigned item = warp * gridDim.x + blockIdx.x;
+
+  while (item < a.S) {
+    const int64_t s = a.order ? a.order[item] : static_cast<int64_t>(item);
+    if (a.active == nullptr || a.active[s] != 0) {
+      const int M = a.m_cur[s];
+      const int64_t doff = a.dict_off[s];
+      const double* Gs = a.G + a.g_off[s];
+      const int ldgs = a.ldg[s];
+      const int cps = max(1, SLOT / ldgs);          // columns per ring slot
+      const int groups = (M + cps - 1) / cps;       // slots per pass over G
+      const double lam1 = a.lam1[s], lam2 = a.lam2[s], tol = a.tol[s];
+      const int max_iters = a.max_iters[s];
+
+      double c[MT];
+#pragma unroll
+      for (int t = 0; t < MT; ++t) {
+        const int k = 32 * t + lane;
+        c[t] = (k < M) ? a.q[doff + k] : 0.0;
+      }
+      const int64_t total = (int64_t)(max_iters + 1) * groups;  // prologue pass + sweeps
+      int64_t issued = 0;
+      int next_group = 0;
+      auto issue_one = [&]() {
+        if (lane == 0) {
+          const int st = g_issue % STAGES;
+          const int c0 = next_group * cps;
+          const int nc = min(cps, M - c0);
+          const uint32_t nb = static_cast<uint32_t>(nc) * ldgs * sizeof(double);
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(&bars[st], nb);
+          tma_load_1d(ring + st * SLOT, Gs + (int64_t)c0 * ldgs, nb, &bars[st]);
+        }
+        ++g_issue;
+        ++issued;
+        if (++next_group == groups) next_group = 0;
+      };
+      for (int q0 = 0; q0 < STAGES && issued < total; ++q0) issue_one();
+      int64_t consumed = 0;
+      const double* slot = nullptr;
+      auto column = [&](int j) -> const double* {
+        const int in = j % cps;
+        if (in == 0) {
+          const int st = g_cons % STAGES;
+          mbar_wait(&bars[st], (g_cons / STAGES) & 1u);
+          ++g_cons;
+          ++consumed;
+          slot = ring + st * SLOT;
+        }
+        return slot + in * ldgs;
+      };
+      auto release = [&](int j) {  // after the last column of a slot
+        if ((j % cps) == cps - 1 || j == M - 1) {
+          __syncwarp();
+          if (issued < total) issue_one();
+        }
+      };
+
+      // prologue: c = q - G beta0 (warm start, adaptive.py:268)
+      for (int j = 0; j < M; ++j) {
+        const double* col = column(j);
+        const double b0 = a.beta[doff + j];
+        if (b0 != 0.0) {
+#pragma unroll
+          for (int t = 0; t < MT; ++t)
+            if (32 * t + lane < M) c[t] = __dsub_rn(c[t], __dmul_rn(b0, col[32 * t + lane]));
+        }
+        release(j);
+      }
+
+      int sweeps_done = 0, conv = 0;
+      for (int sw = 0; sw < max_iters; ++sw) {
+        double max_delta = 0.0, acc_max = 0.0;
+#pragma unroll
+        for (int t = 0; t < MT; ++t) {
+          if (32 * t < M) {
+            const int nc = min(32, M - 32 * t);
+            double bl = 0.0, csl = 0.0;
+            if (lane < nc) {
+              bl = a.beta[doff + 32 * t + lane];
+              csl = a.col_sq[doff + 32 * t + lane];
+            }
+            for (int jj = 0; jj < nc; ++jj) {
+              const int j = 32 * t + jj;
+              const double* col = column(j);
+              const double cj = __shfl_sync(0xffffffffu, c[t], jj);
+              const double b_old = __shfl_sync(0xffffffffu, bl, jj);
+              const double cs = __shfl_sync(0xffffffffu, csl, jj);
+              const double dn = __dadd_rn(cs, lam2);
+              const double z = __dadd_rn(__dmul_rn(cs, b_old), cj);
+              double b_new = 0.0;
+              if (dn > 0.0) {
+                double mag = __dsub_rn(fabs(z), lam1);
+                if (mag < 0.0) mag = 0.0;
+                b_new = __ddiv_rn(z >= 0.0 ? mag : -mag, dn);
+              }
+              if (b_new != b_old) {
+                const double d = __dsub_rn(b_new, b_old);
+#pragma unroll
+                for (int t2 = 0; t2 < MT; ++t2)
+                  if (32 * t2 + lane < M) c[t2] = __dsub_rn(c[t2], __dmul_rn(d, col[32 * t2 + lane]));
+                if (lane == jj) bl = b_new;
+                max_delta = fmax(max_delta, fabs(d));
+              }
+              release(j);
+            }
+            if (lane < nc) {
+              a.beta[doff + 32 * t + lane] = bl;
+              acc_max = fmax(acc_max, fabs(bl));
+            }
+          }
+        }
+        const double mabs = warp_max(acc_max);
+        sweeps_done = sw + 1;
+        if (max_delta <= __dmul_rn(tol, fmax(mabs, 1.0))) {
+          conv = 1;
+          break;
+        }
+      }
+      while (consumed < issued) {  // drain speculative prefetches
+        const int st = g_cons % STAGES;
+        mbar_wait(&bars[st], (g_cons / STAGES) & 1u);
+        ++g_cons;
+        ++consumed;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        a.sweeps[s] = sweeps_done;
+        a.converged[s] = conv;
+      }
+    }
+    unsigned nxt = 0;
+    if (lane == 0) nxt = atomicAdd(&g_gram_queue, 1u) + total_warps;
+    item = __shfl_sync(0xffffffffu, nxt, 0);
+  }
+}
+
+template <int MT, int STAGES, int WPC, int SLOT>
+int launch_gram_cd(const GramArgs& a, cudaStream_t stream) {
+  const size_t smem = static_cast<size_t>(WPC) * STAGES * (SLOT * sizeof(double) + sizeof(uint64_t));
+  static bool configured = false;
+  if (!configured) {
+    PAM_CUDA_CHECK(cudaFuncSetAttribute(cd_gram_kernel<MT, STAGES, WPC, SLOT>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  int dev = 0, sms = 148;
+  PAM_CUDA_CHECK(cudaGetDevice(&dev));
+  PAM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  void* qaddr = nullptr;
+  PAM_CUDA_CHECK(cudaGetSymbolAddress(&qaddr, g_gram_queue));
+  PAM_CUDA_CHECK(cudaMemsetAsync(qaddr, 0, sizeof(unsigned), stream));
+  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(sms, ceil_div(a.S, 1)));
+  cd_gram_kernel<MT, STAGES, WPC, SLOT><<<(unsigned)ctas, WPC * 32, smem, stream>>>(a);
+  PAM_LAUNCH_CHECK("cd_gram_kernel");
+  return PAM_OK;
+}
+
+}  // namespace pam
+
+using namespace pam;
+
+extern "C" int pam_gram_f64(int64_t S, const int64_t* row_off, const int32_t* m_cur,
+                            const int64_t* dict_off, const int64_t* w_off, const int32_t* ld,
+                            const int64_t* g_off, const int32_t* ldg, const int32_t* active,
+                            int32_t max_m, const double* W, const double* y, double* G, double* q,
+                            double* col_sq, void* stream) {
+  if (S < 0 || max_m < 0) return PAM_ERR_ARG;
+  if (S == 0 || max_m == 0) return PAM_OK;
+  cudaStream_t st = as_stream(stream);
+  const int T = (max_m + GT_TILE - 1) / GT_TILE;
+  for (int64_t s0 = 0; s0 < S; s0 += 65535) {
+    const int64_t cnt = std::min<int64_t>(65535, S - s0);
+    const int32_t* act = active ? active + s0 : nullptr;
+    gram_kernel<<<dim3(T * (T + 1) / 2, (unsigned)cnt), 256, 0, st>>>(
+        row_off + s0, m_cur + s0, w_off + s0, ld + s0, g_off + s0, ldg + s0, act, W, G);
+    PAM_LAUNCH_CHECK("gram_kernel");
+    gemv_t_kernel<<<dim3((unsigned)ceil_div((int64_t)max_m * 32, 256), (unsigned)cnt), 256, 0, st>>>(
+        row_off + s0, m_cur + s0, dict_off + s0, w_off + s0, ld + s0, g_off + s0, ldg + s0, act, W,
+        y, G, q, col_sq);
+    PAM_LAUNCH_CHECK("gemv_t_kernel");
+  }
+  return PAM_OK;
+}
+
+extern "C" int pam_cd_gram_f64(int64_t S, const int64_t* order, const int64_t* dict_off,
+                               const int32_t* m_cur, const int64_t* g_off, const int32_t* ldg,
+                               const double* G, const double* q, const double* col_sq,
+                               const double* lam1, const double* lam2, const double* tol,
+                               const int32_t* max_iters, const int32_t* active, int32_t max_m,
+                               double* beta, int32_t* sweeps, int32_t* converged, void* stream) {
+  if (S < 0 || max_m < 0) return PAM_ERR_ARG;
+  if (S == 0) return PAM_OK;
+  GramArgs a{S, order, dict_off, m_cur, g_off, ldg, G, q, col_sq, lam1, lam2, tol, max_iters,
+             active, beta, sweeps, converged};
+  cudaStream_t st = as_stream(stream);
+  // ldg <= SLOT is required: ldg = M_cap rounded to 16
+  if (max_m <= 64) return launch_gram_cd<2, 4, 24, 512>(a, st);
+  if (max_m <= 128) return launch_gram_cd<4, 4, 16, 512>(a, st);
+  if (max_m <= 256) return launch_gram_cd<8, 3, 16, 512>(a, st);
+  if (max_m <= 512) return launch_gram_cd<16, 3, 16, 512>(a, st);
+  set_last_error("pam_cd_gram_f64: Gram-form CD supports M <= 512 (use the residual form)");
+  return PAM_ERR_UNSUPPORTED;
+}

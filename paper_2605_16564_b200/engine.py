@@ -175,6 +175,36 @@ def rcb_permutation(points: np.ndarray, leaf: int = 32) -> np.ndarray:
     return out
 
 
+GRAM_MAX_M = 512
+
+
+def cd_form(n_rows, cap) -> str:
+    """Which CD formulation streams fewer bytes for this batch.
+
+    Residual form streams N*M doubles per sweep, the covariance (Gram) form
+    M*M (hard part 1); the Gram kernel keeps c in registers and
+    supports M <= 512.  Env PAM_CD_FORM = auto | residual | gram.
+    """
+    import os
+
+    forced = os.environ.get("PAM_CD_FORM", "auto")
+    cap = np.asarray(cap, dtype=np.int64)
+    fits = int(cap.max()) <= GRAM_MAX_M
+    if forced == "gram" and fits:
+        return "gram"
+    if forced == "residual" or not fits:
+        return "residual"
+    return "gram" if np.all(cap * 4 <= np.asarray(n_rows) * 3) else "residual"
+
+
+def device_bytes(n_rows, cap) -> np.ndarray:
+    """Per-subdomain HBM for design matrices (+ Gram matrices) in one device batch."""
+    n_rows = np.asarray(n_rows, dtype=np.int64)
+    cap = np.asarray(cap, dtype=np.int64)
+    w = (n_rows + 31) // 32 * 32 * cap * 8
+    return w + np.where(cap <= GRAM_MAX_M, _round16(cap) * cap * 8, 0)
+
+
 def estimate_w_bytes(n_rows, cap):
     return int(np.sum(_round16(n_rows) * np.asarray(cap, dtype=np.int64)) * 8)
 
@@ -224,8 +254,9 @@ class FitEngine:
         self.cap = dictionary_capacity(m0, p["k_top"], p["m_q"], p["m_max"], p["max_rounds"])
         self.dict_off = np.concatenate([[0], np.cumsum(self.cap)[:-1]]).astype(np.int64)
         cap_tot = int(self.cap.sum())
+        self.form = cd_form(self.n_rows, self.cap)
         self.tau = tile_tau() if tau is None else float(tau)
-        self.tiles = self.tau > 0.0 and self.max_rows <= 1024
+        self.tiles = self.form == "residual" and self.tau > 0.0 and self.max_rows <= 1024
         self.ld = _round16(self.n_rows) if not self.tiles else (self.n_rows + 31) // 32 * 32
         wsz = self.ld * self.cap
         self.w_off = np.concatenate([[0], np.cumsum(wsz)[:-1]]).astype(np.int64)
@@ -279,6 +310,18 @@ class FitEngine:
         self.d_qoff = nat.to_dev(np.concatenate([q1o, q2o]).reshape(-1))
         self.d_qw = nat.to_dev(np.concatenate([q1w, q2w]))
         self.err = nat.ErrorWord()
+        if self.form == "gram":
+            self.ldg = _round16(self.cap)
+            gsz = self.ldg * self.cap
+            self.g_off = np.concatenate([[0], np.cumsum(gsz)[:-1]]).astype(np.int64)
+            self.d_G = t.empty(int(gsz.sum()), dtype=f64, device=dev)
+            self.d_g_off = nat.to_dev(self.g_off)
+            self.d_ldg = nat.to_dev(self.ldg.astype(np.int32))
+            self.d_q = t.empty(cap_tot, dtype=f64, device=dev)
+            self.d_zero_iters = t.zeros(S, dtype=i32, device=dev)
+            self.d_obj_sweeps = t.zeros(S, dtype=i32, device=dev)
+            self.d_obj_conv = t.zeros(S, dtype=i32, device=dev)
+            self.d_obj_colsq = t.empty(cap_tot, dtype=f64, device=dev)
         if self.tiles:
             self.d_perm = None if row_perm is None else nat.to_dev(np.asarray(row_perm, dtype=np.int32))
             self.d_rowmax = t.empty(ntot, dtype=f64, device=dev)
@@ -360,7 +403,25 @@ class FitEngine:
                     P(self.d_centres), P(self.d_widths), P(self.d_w_off), P(self.d_ld), P(self.d_active),
                     self.max_rows, 0, P(self.d_W), st), "pam_assemble_f64")
             e1.record()
-            if self.tiles:
+            if self.form == "gram":
+                max_m = int(self.m_cur.max())
+                nat.check(lib.pam_gram_f64(
+                    S, P(self.d_row_off), P(self.d_m_cur), P(self.d_dict_off), P(self.d_w_off),
+                    P(self.d_ld), P(self.d_g_off), P(self.d_ldg), P(self.d_active), max_m, P(self.d_W),
+                    P(self.d_y), P(self.d_G), P(self.d_q), P(self.d_col_sq), st), "pam_gram_f64")
+                nat.check(lib.pam_cd_gram_f64(
+                    len(order), P(d_order), P(self.d_dict_off), P(self.d_m_cur), P(self.d_g_off),
+                    P(self.d_ldg), P(self.d_G), P(self.d_q), P(self.d_col_sq), P(self.d_lam1),
+                    P(self.d_lam2), P(self.d_tol), P(self.d_max_iters), P(self.d_active), max_m,
+                    P(self.d_beta), P(self.d_sweeps), P(self.d_conv), st), "pam_cd_gram_f64")
+                # exact objective at the final beta: residual form with zero sweeps
+                nat.check(lib.pam_cd_f64(
+                    len(order), P(d_order), P(self.d_row_off), P(self.d_y), P(self.d_dict_off),
+                    P(self.d_m_cur), P(self.d_w_off), P(self.d_ld), P(self.d_W), P(self.d_lam1),
+                    P(self.d_lam2), P(self.d_tol), P(self.d_zero_iters), P(self.d_active),
+                    self.max_rows, P(self.d_beta), P(self.d_obj_colsq), P(self.d_obj_sweeps),
+                    P(self.d_obj_conv), P(self.d_obj), None, None, st), "pam_cd_f64")
+            elif self.tiles:
                 nat.check(lib.pam_cd_tiles_f64(
                     len(order), P(d_order), P(self.d_row_off), P(self.d_y), P(self.d_perm),
                     P(self.d_dict_off), P(self.d_m_cur), P(self.d_w_off), P(self.d_tile_mask),
@@ -388,7 +449,9 @@ class FitEngine:
             obj = self.d_obj.cpu().numpy()
             sweeps = self.d_sweeps.cpu().numpy()
             conv = self.d_conv.cpu().numpy()
-            if self.tiles:
+            if self.form == "gram":
+                stream_doubles = self.m_cur * self.m_cur  # one G column per coordinate
+            elif self.tiles:
                 stream_doubles = self.d_packed.cpu().numpy()
             else:
                 stream_doubles = self.n_rows * self.m_cur
@@ -563,7 +626,7 @@ def fit_packed(dim, row_off, points, values, box_lo, box_hi, configs, dict_m, ce
     k_top = np.minimum([c.k_top for c in configs], n_rows)
     cap = dictionary_capacity(dict_m, k_top, [c.m_q for c in configs], [c.m_max for c in configs],
                               [c.max_rounds for c in configs])
-    chunks = chunk_ranges(_round16(n_rows) * cap * 8, budget or w_budget_bytes())
+    chunks = chunk_ranges(device_bytes(n_rows, cap), budget or w_budget_bytes())
     points = np.asarray(points, dtype=np.float64).reshape(-1, dim)
     values = np.asarray(values, dtype=np.float64).reshape(-1)
     centres = np.asarray(centres, dtype=np.float64).reshape(-1, dim)

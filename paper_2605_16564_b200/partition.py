@@ -467,8 +467,8 @@ def fit_subset(data: FieldData, partition: Partition, cfgs, specs, lo: int, hi: 
 
 def _fit_range(data, partition, cfgs, specs, lo, hi):
     """Device fits of subdomains [lo, hi): (locals, rounds, seconds, device parts, stats, max batch)."""
-    from .engine import (EngineError, FitEngine, chunk_ranges, dictionary_capacity, reports_for,
-                         w_budget_bytes)
+    from .engine import (EngineError, FitEngine, chunk_ranges, device_bytes, dictionary_capacity,
+                         reports_for, w_budget_bytes)
 
     mesh = partition.mesh
     dim = mesh.dim
@@ -506,7 +506,7 @@ def _fit_range(data, partition, cfgs, specs, lo, hi):
     k_top = np.minimum([c.k_top for c in cfgs[lo:hi]], n_rows[lo:hi])
     cap = dictionary_capacity(m0, k_top, [c.m_q for c in cfgs[lo:hi]], [c.m_max for c in cfgs[lo:hi]],
                               [c.max_rounds for c in cfgs[lo:hi]])
-    wbytes = (n_rows[lo:hi] + 31) // 32 * 32 * cap * 8
+    wbytes = device_bytes(n_rows[lo:hi], cap)
     chunks = [(lo + a, lo + b) for a, b in chunk_ranges(wbytes, w_budget_bytes())]
     n = hi - lo
 
