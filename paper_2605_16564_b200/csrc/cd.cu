@@ -70,7 +70,7 @@ __device__ __forceinline__ void group_bar(int id, int nthreads) {
 
 // R: rows per thread, STAGES: ring depth, WPC: warps per CTA, G: warps per
 // subdomain group (rows of a subdomain split over the G*32 threads).
-template <int R, int STAGES, int WPC, int G, bool TILES>
+template <int R, int STAGES, int WPC, int G, bool TILES, bool KEEPW = true>
 __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
   static_assert(!TILES || G == 1, "tile-packed columns are consumed one warp per subdomain");
   constexpr int GT = G * 32;         // threads per group
@@ -165,13 +165,14 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
             iss_off_l = (c < M) ? a.col_off[doff + c] : 0;
             iss_mask_l = (c < M) ? a.tile_mask[doff + c] : 0ull;
           }
-          const int64_t off = __shfl_sync(0xffffffffu, iss_off_l, next_col & 31);
-          const unsigned long long mk = __shfl_sync(0xffffffffu, iss_mask_l, next_col & 31);
+          const int off = __shfl_sync(0xffffffffu, static_cast<int>(iss_off_l), next_col & 31);
+          unsigned long long mk;
+          if (R <= 32) mk = __shfl_sync(0xffffffffu, static_cast<unsigned>(iss_mask_l), next_col & 31);
+          else mk = __shfl_sync(0xffffffffu, iss_mask_l, next_col & 31);
           const uint32_t nb = static_cast<uint32_t>(__popcll(mk)) * 32u * sizeof(double);
           if (lane == 0) {
             const int st = g_issue % STAGES;
             if (nb) {
-              fence_proxy_async_smem();
               mbar_arrive_expect_tx(&bars[st], nb);
               tma_load_1d(ring + st * LDMAX, Ws + off, nb, &bars[st]);
             } else {
@@ -180,7 +181,6 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
           }
         } else if (gt == 0) {
           const int st = g_issue % STAGES;
-          fence_proxy_async_smem();
           mbar_arrive_expect_tx(&bars[st], dense_bytes);
           tma_load_1d(ring + st * LDMAX, Ws + (int64_t)next_col * ld, dense_bytes, &bars[st]);
         }
@@ -198,16 +198,45 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
       // registers once and serve both the dot and the AXPY.  Branch-free: rows
       // past N (dense) or tiles not stored (tile mode) read an in-bounds smem
       // word and select 0, so they contribute exactly nothing.
-      double w[R];
+      double w[KEEPW ? R : 1];
+      const double* cur_col = nullptr;
+      unsigned long long cur_mk = 0ull;
       auto load_col = [&](const double* col, unsigned long long mk) {
+        cur_col = col;
+        cur_mk = mk;
+        if (!KEEPW) return;
         if (TILES) {
+          // Tiles in groups of four with warp-uniform fast paths: RCB ordering
+          // makes kept tiles cluster, so most groups are all-kept (contiguous
+          // loads, no selects) or all-dropped (zeros).
           int slot = 0;
 #pragma unroll
-          for (int k = 0; k < R; ++k) {
-            const int bit = static_cast<int>((mk >> k) & 1ull);
-            const double v = col[32 * slot + lane];  // slot <= k < R: inside the ring slot
-            w[k] = bit ? v : 0.0;
-            slot += bit;
+          for (int g = 0; g < (R + 3) / 4; ++g) {
+            constexpr int dummy = 0;
+            (void)dummy;
+            const int cnt = (4 * g + 4 <= R) ? 4 : (R - 4 * g);
+            const unsigned full = (1u << cnt) - 1u;
+            const unsigned nib = static_cast<unsigned>(mk >> (4 * g)) & full;
+            if (nib == full) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (u < cnt) w[4 * g + u] = col[32 * (slot + u) + lane];
+              slot += cnt;
+            } else if (nib == 0u) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (u < cnt) w[4 * g + u] = 0.0;
+            } else {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                if (u < cnt) {
+                  const int bit = static_cast<int>((nib >> u) & 1u);
+                  const double v = col[32 * slot + lane];  // slot <= k < R: inside the ring slot
+                  w[4 * g + u] = bit ? v : 0.0;
+                  slot += bit;
+                }
+              }
+            }
           }
         } else {
 #pragma unroll
@@ -217,15 +246,43 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
           }
         }
       };
+      // entry k of the current column for this thread (0 when absent)
+      auto wk = [&](int k, int& slot) -> double {
+        if (KEEPW) return w[KEEPW ? k : 0];
+        if (TILES) {
+          const int bit = static_cast<int>((cur_mk >> k) & 1ull);
+          const double v = cur_col[32 * slot + lane];
+          slot += bit;
+          return bit ? v : 0.0;
+        }
+        const double v = cur_col[gt + GT * k];
+        return (gt + GT * k < N) ? v : 0.0;
+      };
       auto col_dot = [&]() -> double {
-        double dot = 0.0;
+        double d0 = 0.0, d1 = 0.0;  // two independent chains halve the FMA latency
+        int slot = 0;
 #pragma unroll
-        for (int k = 0; k < R; ++k) dot = fma(w[k], r[k], dot);
-        return dot;
+        for (int k = 0; k < R; ++k) {
+          const double v = wk(k, slot);
+          if (k & 1) d1 = fma(v, r[k], d1);
+          else d0 = fma(v, r[k], d0);
+        }
+        return d0 + d1;
       };
       auto col_axpy = [&](double d) {
+        int slot = 0;
 #pragma unroll
-        for (int k = 0; k < R; ++k) r[k] = fma(-d, w[k], r[k]);
+        for (int k = 0; k < R; ++k) r[k] = fma(-d, wk(k, slot), r[k]);
+      };
+      auto col_sumsq = [&]() -> double {
+        double p = 0.0;
+        int slot = 0;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          const double v = wk(k, slot);
+          p = fma(v, v, p);
+        }
+        return p;
       };
       for (int q = 0; q < STAGES && issued < total; ++q) issue_one();
       int64_t consumed = 0;
@@ -243,10 +300,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
             ++consumed;
             load_col(col, mk);
             if (need_colsq) {
-              double p = 0.0;
-#pragma unroll
-              for (int k = 0; k < R; ++k) p = fma(w[k], w[k], p);
-              p = group_sum(p);
+              double p = group_sum(col_sumsq());
               if (gt == 0) a.col_sq[doff + j] = p;
             }
             if (!r_given) {
@@ -279,7 +333,11 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
             if (TILES) ml = a.tile_mask[doff + cb + lane];
           }
           for (int t = 0; t < nc; ++t) {
-            const unsigned long long mk = TILES ? __shfl_sync(0xffffffffu, ml, t) : 0ull;
+            unsigned long long mk = 0ull;
+            if (TILES) {
+              if (R <= 32) mk = __shfl_sync(0xffffffffu, static_cast<unsigned>(ml), t);
+              else mk = __shfl_sync(0xffffffffu, ml, t);
+            }
             const double* col = wait_one();
             ++consumed;
             load_col(col, mk);
@@ -377,7 +435,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
   }
 }
 
-template <int R, int STAGES, int WPC, int G, bool TILES = false>
+template <int R, int STAGES, int WPC, int G, bool TILES = false, bool KEEPW = true>
 int launch_cd(const CdArgs& a, cudaStream_t stream) {
   constexpr int NGROUPS = WPC / G;
   const size_t smem = static_cast<size_t>(NGROUPS) * STAGES * (R * 32 * G * sizeof(double)) +
@@ -385,7 +443,7 @@ int launch_cd(const CdArgs& a, cudaStream_t stream) {
                       static_cast<size_t>(NGROUPS) * (2 * G + 1) * sizeof(double);
   static bool configured = false;
   if (!configured) {
-    PAM_CUDA_CHECK(cudaFuncSetAttribute(cd_kernel<R, STAGES, WPC, G, TILES>,
+    PAM_CUDA_CHECK(cudaFuncSetAttribute(cd_kernel<R, STAGES, WPC, G, TILES, KEEPW>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
@@ -396,7 +454,7 @@ int launch_cd(const CdArgs& a, cudaStream_t stream) {
   PAM_CUDA_CHECK(cudaGetSymbolAddress(&qaddr, g_cd_queue));
   PAM_CUDA_CHECK(cudaMemsetAsync(qaddr, 0, sizeof(unsigned), stream));
   const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(sms, a.S));
-  cd_kernel<R, STAGES, WPC, G, TILES><<<(unsigned)ctas, WPC * 32, smem, stream>>>(a);
+  cd_kernel<R, STAGES, WPC, G, TILES, KEEPW><<<(unsigned)ctas, WPC * 32, smem, stream>>>(a);
   PAM_LAUNCH_CHECK("cd_kernel");
   return PAM_OK;
 }
@@ -435,7 +493,9 @@ int cd_dispatch_tiles(const CdArgs& a, int max_rows, cudaStream_t stream) {
   if (max_rows <= 256) return launch_cd<8, 4, 16, 1, true>(a, stream);
   if (max_rows <= 512) {
     static const char* env = getenv("PAM_CD_WPC16");
-    if (env && atoi(env) == 12) return launch_cd<16, 3, 12, 1, true>(a, stream);
+    const int v = env ? atoi(env) : 16;
+    if (v == 24) return launch_cd<16, 2, 24, 1, true, false>(a, stream);
+    if (v == 20) return launch_cd<16, 2, 20, 1, true, false>(a, stream);
     return launch_cd<16, 3, 16, 1, true>(a, stream);
   }
   if (max_rows <= 1024) return launch_cd<32, 3, 8, 1, true>(a, stream);

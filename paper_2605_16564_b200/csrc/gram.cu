@@ -347,8 +347,8 @@ extern "C" int pam_cd_gram_f64(int64_t S, const int64_t* order, const int64_t* d
              active, beta, sweeps, converged};
   cudaStream_t st = as_stream(stream);
   // ldg <= SLOT is required: ldg = M_cap rounded to 16
-  if (max_m <= 64) return launch_gram_cd<2, 4, 24, 512>(a, st);
-  if (max_m <= 128) return launch_gram_cd<4, 4, 16, 512>(a, st);
+  if (max_m <= 64) return launch_gram_cd<2, 3, 24, 256>(a, st);
+  if (max_m <= 128) return launch_gram_cd<4, 3, 16, 512>(a, st);
   if (max_m <= 256) return launch_gram_cd<8, 3, 16, 512>(a, st);
   if (max_m <= 512) return launch_gram_cd<16, 3, 16, 512>(a, st);
   set_last_error("pam_cd_gram_f64: Gram-form CD supports M <= 512 (use the residual form)");

@@ -234,6 +234,28 @@ def test_tile_packed_stream_matches_dense(cuda, monkeypatch, cells):
             assert abs(x.rel_l2 - y.rel_l2) <= 1e-10 * x.rel_l2
 
 
+def test_gram_form_matches_residual_form(cuda, monkeypatch):
+    """Covariance-form CD (gram.cu) vs residual form on a lattice dictionary with refinement."""
+    field = pam.box_field_2d(32, 32)
+    part = pam.make_partition(field.mesh, 2, 2)
+    cfg = pam.AdaptiveConfig(k_top=16, m_max=96, m_q=3, max_rounds=3, elastic=EN_2D,
+                             offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
+    spec = pam.DictionarySpec(sigma=1.0 / 16, lattice=8)  # M0=64, cap=160 < 0.75*N=192
+    monkeypatch.setenv("PAM_CD_FORM", "residual")
+    res, rr = pam.fit_parallel(field, part, cfg, spec)
+    monkeypatch.setenv("PAM_CD_FORM", "gram")
+    gram, rg = pam.fit_parallel(field, part, cfg, spec)
+    assert rg.device["cd_bytes"] < rr.device["cd_bytes"]
+    for a, b in zip(res.locals, gram.locals):
+        np.testing.assert_array_equal(a.dictionary.centers, b.dictionary.centers)
+        assert np.max(np.abs(a.beta - b.beta)) <= 1e-9 * max(1, np.abs(a.beta).max())
+    for ra, rb in zip(rr.rounds, rg.rounds):
+        for x, y in zip(ra, rb):
+            assert (x.centers, x.added) == (y.centers, y.added)
+            assert abs(x.objective - y.objective) <= 1e-9 * abs(x.objective)
+            assert abs(x.rel_l2 - y.rel_l2) <= 1e-9 * x.rel_l2
+
+
 class _BrokenSpec(pam.DictionarySpec):
     def build(self, sub):
         raise RuntimeError("boom")
