@@ -525,6 +525,14 @@ extern "C" int pam_cd_ex_f64(int64_t S, const int64_t* order, const int64_t* row
   return cd_dispatch(a, max_rows, as_stream(stream));
 }
 
+int pam_cd_tiles_ring(int64_t S, const int64_t* order, const int64_t* row_off, const double* y,
+                      const int32_t* perm, const int64_t* dict_off, const int32_t* m_cur,
+                      const int64_t* w_off, const uint64_t* tile_mask, const int64_t* col_off,
+                      const double* W, const double* lam1, const double* lam2, const double* tol,
+                      const int32_t* max_iters, const int32_t* active, int32_t max_rows,
+                      double* beta, double* col_sq, int32_t* sweeps, int32_t* converged,
+                      double* objective, void* stream);
+
 extern "C" int pam_cd_tiles_f64(int64_t S, const int64_t* order, const int64_t* row_off,
                                 const double* y, const int32_t* perm, const int64_t* dict_off,
                                 const int32_t* m_cur, const int64_t* w_off,
@@ -536,6 +544,11 @@ extern "C" int pam_cd_tiles_f64(int64_t S, const int64_t* order, const int64_t* 
                                 void* stream) {
   if (S < 0 || max_rows < 0 || !tile_mask || !col_off) return PAM_ERR_ARG;
   if (S == 0) return PAM_OK;
+  static const char* ring_env = getenv("PAM_CD_RING");
+  if (hist == nullptr && max_rows <= 1024 && !(ring_env && atoi(ring_env) == 0))
+    return pam_cd_tiles_ring(S, order, row_off, y, perm, dict_off, m_cur, w_off, tile_mask, col_off,
+                             W, lam1, lam2, tol, max_iters, active, max_rows, beta, col_sq, sweeps,
+                             converged, objective, stream);
   CdArgs a{S,      order,     row_off,   const_cast<double*>(y), dict_off, m_cur, w_off, m_cur,
            W,      lam1,      lam2,      tol,       max_iters, active, beta,   col_sq,
            sweeps, converged, objective, hist,      hist_off,  0,

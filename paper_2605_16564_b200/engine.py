@@ -635,8 +635,11 @@ def fit_packed(dim, row_off, points, values, box_lo, box_hi, configs, dict_m, ce
     for a, b in chunks:
         r0, r1 = int(row_off[a]), int(row_off[b])
         m0, m1 = int(m_off[a]), int(m_off[b])
+        # the CD row order only matters for the tile-packed stream
+        use_tiles = (cd_form(n_rows[a:b], cap[a:b]) == "residual" and tile_tau() > 0
+                     and int(n_rows[a:b].max()) <= 1024)
         perm = np.concatenate([rcb_permutation(points[row_off[i]:row_off[i + 1]])
-                               for i in range(a, b)]) if b - a <= 8192 else None
+                               for i in range(a, b)]) if use_tiles and b - a <= 16384 else None
         try:
             eng = FitEngine(dim, cell_size, row_off[a:b + 1] - r0, nat.to_dev(points[r0:r1].reshape(-1)),
                             nat.to_dev(values[r0:r1]), np.asarray(box_lo)[a:b], np.asarray(box_hi)[a:b],
