@@ -545,7 +545,7 @@ extern "C" int pam_cd_tiles_f64(int64_t S, const int64_t* order, const int64_t* 
   if (S < 0 || max_rows < 0 || !tile_mask || !col_off) return PAM_ERR_ARG;
   if (S == 0) return PAM_OK;
   static const char* ring_env = getenv("PAM_CD_RING");
-  if (hist == nullptr && max_rows <= 1024 && !(ring_env && atoi(ring_env) == 0))
+  if (hist == nullptr && max_rows <= 1024 && ring_env && atoi(ring_env) == 1)
     return pam_cd_tiles_ring(S, order, row_off, y, perm, dict_off, m_cur, w_off, tile_mask, col_off,
                              W, lam1, lam2, tol, max_iters, active, max_rows, beta, col_sq, sweeps,
                              converged, objective, stream);
