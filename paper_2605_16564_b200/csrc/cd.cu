@@ -92,6 +92,15 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
                     NGROUPS * STAGES) +
                 grp * (2 * G + 1);  // double-buffered cross-warp partials + queue slot
   const int bar_id = 1 + grp;
+  // per-warp column-parameter block (G == 1): beta, col_sq, tile mask of the
+  // current 32-column chunk, read by warp-uniform smem broadcasts
+  constexpr bool PSM = (G == 1);
+  double* prm_base = reinterpret_cast<double*>(smem_raw) +
+                     (static_cast<size_t>(NGROUPS) * STAGES * LDMAX) + NGROUPS * STAGES +
+                     NGROUPS * (2 * G + 1);
+  double* pb = prm_base + grp * 96;
+  double* pc = pb + 32;
+  unsigned* pm = reinterpret_cast<unsigned*>(pb + 64);
 
   auto sync_group = [&]() {
     if (G == 1) __syncwarp();
@@ -327,7 +336,15 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
           // every warp of the group holds the same 32 column parameters
           double bl = 0.0, csl = 0.0;
           unsigned long long ml = 0ull;
-          if (lane < nc) {
+          if (PSM) {
+            __syncwarp();
+            if (lane < nc) {
+              pb[lane] = a.beta[doff + cb + lane];
+              pc[lane] = a.col_sq[doff + cb + lane];
+              if (TILES) pm[lane] = static_cast<unsigned>(a.tile_mask[doff + cb + lane]);
+            }
+            __syncwarp();
+          } else if (lane < nc) {
             bl = a.beta[doff + cb + lane];
             csl = a.col_sq[doff + cb + lane];
             if (TILES) ml = a.tile_mask[doff + cb + lane];
@@ -335,15 +352,16 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
           for (int t = 0; t < nc; ++t) {
             unsigned long long mk = 0ull;
             if (TILES) {
-              if (R <= 32) mk = __shfl_sync(0xffffffffu, static_cast<unsigned>(ml), t);
+              if (PSM) mk = pm[t];
+              else if (R <= 32) mk = __shfl_sync(0xffffffffu, static_cast<unsigned>(ml), t);
               else mk = __shfl_sync(0xffffffffu, ml, t);
             }
             const double* col = wait_one();
             ++consumed;
             load_col(col, mk);
             const double dot = group_sum(col_dot());
-            const double b_old = __shfl_sync(0xffffffffu, bl, t);
-            const double cs = __shfl_sync(0xffffffffu, csl, t);
+            const double b_old = PSM ? pb[t] : __shfl_sync(0xffffffffu, bl, t);
+            const double cs = PSM ? pc[t] : __shfl_sync(0xffffffffu, csl, t);
             const double dn = __dadd_rn(cs, lam2);
             const double z = __dadd_rn(__dmul_rn(cs, b_old), dot);
             double b_new = 0.0;
@@ -352,14 +370,22 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
               if (mag < 0.0) mag = 0.0;
               b_new = __ddiv_rn(z >= 0.0 ? mag : -mag, dn);
             }
-            if (b_new != b_old) {
-              const double d = __dsub_rn(b_new, b_old);
-              col_axpy(d);
-              if (lane == t) bl = b_new;
-              max_delta = fmax(max_delta, fabs(d));
+            // branch-free update: d == 0 exactly when b_new == b_old, and then the
+            // AXPY adds -0 * w to every residual entry, leaving r bit-unchanged
+            const double d = __dsub_rn(b_new, b_old);
+            col_axpy(d);
+            if (PSM) {
+              if (lane == 0) pb[t] = b_new;
+            } else if (lane == t) {
+              bl = b_new;
             }
+            max_delta = fmax(max_delta, fabs(d));
             sync_group();
             if (issued < total) issue_one();
+          }
+          if (PSM) {
+            __syncwarp();
+            bl = (lane < nc) ? pb[lane] : 0.0;
           }
           if (lane < nc) {
             if (wig == 0) a.beta[doff + cb + lane] = bl;
@@ -440,7 +466,8 @@ int launch_cd(const CdArgs& a, cudaStream_t stream) {
   constexpr int NGROUPS = WPC / G;
   const size_t smem = static_cast<size_t>(NGROUPS) * STAGES * (R * 32 * G * sizeof(double)) +
                       static_cast<size_t>(NGROUPS) * STAGES * sizeof(uint64_t) +
-                      static_cast<size_t>(NGROUPS) * (2 * G + 1) * sizeof(double);
+                      static_cast<size_t>(NGROUPS) * (2 * G + 1) * sizeof(double) +
+                      static_cast<size_t>(NGROUPS) * 96 * sizeof(double);
   static bool configured = false;
   if (!configured) {
     PAM_CUDA_CHECK(cudaFuncSetAttribute(cd_kernel<R, STAGES, WPC, G, TILES, KEEPW>,
