@@ -57,6 +57,7 @@ template <int R, int WPC, int RB, int NB>
 __global__ void __launch_bounds__(WPC * 32, 1) cd_tiles_kernel(const CdTilesArgs a) {
   static_assert(R <= 32, "32-bit tile masks");
   static_assert(RB >= 32 * R, "a full column must fit the ring");
+  static_assert((NB & (NB - 1)) == 0, "NB must be a power of two");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -93,24 +94,21 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tiles_kernel(const CdTilesArgs
         r[k] = (p < N) ? a.y[r0 + row] : 0.0;
       }
 
-      // producer state
+      // producer state (physical ring positions, 32-bit, no modulo)
       const int64_t total = (int64_t)(max_iters + 1) * M;  // prologue pass + sweeps
       int64_t issued = 0;
       int p_col = 0;
-      int64_t p_pos = 0;          // virtual ring position of the next column
+      int p_phys = 0;   // physical start of the next column
+      int in_use = 0;   // doubles held by unreleased columns, including wrap waste
       int iss_base = -64;
       int iss_off_l = 0;
       unsigned iss_mask_l = 0u;
-      // consumer state (replays the allocation rule)
-      int64_t c_pos = 0;          // virtual start of the oldest unreleased column
+      // consumer state (replays the placement rule)
+      int c_phys = 0;
       int64_t consumed = 0;
 
-      auto place = [&](int64_t pos, int nd) -> int64_t {
-        const int64_t phys = pos % RB;
-        return (phys + nd > RB) ? pos + (RB - phys) : pos;
-      };
       auto try_issue = [&]() {
-        while (issued < total && (int64_t)(seq_issue - seq_cons) < NB) {
+        while (issued < total && (seq_issue - seq_cons) < (uint32_t)NB) {
           const int cbase = p_col & ~31;
           if (cbase != iss_base) {  // warp-uniform reload of 32 columns' packing
             iss_base = cbase;
@@ -120,36 +118,40 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tiles_kernel(const CdTilesArgs
           }
           const unsigned mk = __shfl_sync(0xffffffffu, iss_mask_l, p_col & 31);
           const int nd = 32 * __popc(mk);
-          const int64_t start = place(p_pos, nd);
-          if (start + nd > c_pos + RB) break;  // ring full until the consumer releases
+          const int waste = (p_phys + nd > RB) ? RB - p_phys : 0;
+          if (in_use + waste + nd > RB) break;  // ring full until the consumer releases
+          const int start = waste ? 0 : p_phys;
           const int off = __shfl_sync(0xffffffffu, iss_off_l, p_col & 31);
           if (lane == 0) {
-            uint64_t* bar = &bars[seq_issue % NB];
+            uint64_t* bar = &bars[seq_issue & (NB - 1)];
             if (nd) {
               mbar_arrive_expect_tx(bar, static_cast<uint32_t>(nd) * sizeof(double));
-              tma_load_1d(ring + (start % RB), Ws + off, static_cast<uint32_t>(nd) * sizeof(double), bar);
+              tma_load_1d(ring + start, Ws + off, static_cast<uint32_t>(nd) * sizeof(double), bar);
             } else {
               mbar_arrive(bar);
             }
           }
-          p_pos = start + nd;
+          p_phys = start + nd;
+          in_use += waste + nd;
           ++seq_issue;
           ++issued;
           if (++p_col == M) p_col = 0;
         }
       };
       // consume the next column (mask mk): returns its smem base; release() after use
-      int64_t cur_start = 0;
-      int cur_nd = 0;
+      int cur_nd = 0, cur_free = 0;
       auto acquire = [&](unsigned mk) -> const double* {
         cur_nd = 32 * __popc(mk);
-        cur_start = place(c_pos, cur_nd);
-        mbar_wait(&bars[seq_cons % NB], (seq_cons / NB) & 1u);
-        return ring + (cur_start % RB);
+        const int waste = (c_phys + cur_nd > RB) ? RB - c_phys : 0;
+        const int start = waste ? 0 : c_phys;
+        cur_free = waste + cur_nd;
+        c_phys = start + cur_nd;
+        mbar_wait(&bars[seq_cons & (NB - 1)], (seq_cons / NB) & 1u);
+        return ring + start;
       };
       auto release = [&]() {
         __syncwarp();
-        c_pos = cur_start + cur_nd;
+        in_use -= cur_free;
         ++seq_cons;
         ++consumed;
         try_issue();
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tiles_kernel(const CdTilesArgs
       }
       // drain copies of the sweep that will not run
       while (seq_cons < seq_issue) {
-        mbar_wait(&bars[seq_cons % NB], (seq_cons / NB) & 1u);
+        mbar_wait(&bars[seq_cons & (NB - 1)], (seq_cons / NB) & 1u);
         ++seq_cons;
       }
       __syncwarp();
@@ -334,9 +336,14 @@ int pam_cd_tiles_ring(int64_t S, const int64_t* order, const int64_t* row_off, c
                 max_iters, active, beta, col_sq, sweeps, converged, objective};
   cudaStream_t st = as_stream(stream);
   // ring sized so WPC * RB doubles ~ 200 KB per SM; NB mbarriers per warp
-  if (max_rows <= 128) return launch_cd_tiles<4, 16, 1536, 12>(a, st);
-  if (max_rows <= 256) return launch_cd_tiles<8, 16, 1536, 12>(a, st);
-  if (max_rows <= 512) return launch_cd_tiles<16, 16, 1600, 12>(a, st);
-  if (max_rows <= 1024) return launch_cd_tiles<32, 8, 3200, 12>(a, st);
+  static const char* env = getenv("PAM_RING_WPC");
+  const int wpc = env ? atoi(env) : 16;
+  if (max_rows <= 128) return launch_cd_tiles<4, 16, 1536, 16>(a, st);
+  if (max_rows <= 256) return launch_cd_tiles<8, 16, 1536, 16>(a, st);
+  if (max_rows <= 512) {
+    if (wpc == 12) return launch_cd_tiles<16, 12, 2048, 16>(a, st);
+    return launch_cd_tiles<16, 16, 1568, 16>(a, st);
+  }
+  if (max_rows <= 1024) return launch_cd_tiles<32, 8, 3136, 16>(a, st);
   return PAM_ERR_UNSUPPORTED;
 }
