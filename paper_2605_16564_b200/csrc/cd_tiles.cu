@@ -13,11 +13,11 @@
 // dense stream that saturates HBM.
 //
 // Ring rule (replayed identically by producer and consumer, so the consumer
-// never needs the producer's addresses): column q of size nd doubles starts
-// at virtual position p (monotonic); if it would straddle the physical end
-// of the ring it starts at the next multiple of RB instead.  A column may be
-// issued when it ends at most RB past the start of the oldest column not yet
-// released and fewer than NB columns are in flight.
+// never needs the producer's addresses): a column of nd doubles starts at the
+// current physical position p unless p + nd > RB, in which case it starts at
+// 0 and the RB - p tail is wasted; the producer may issue while the doubles
+// held by unreleased columns (plus waste) stay <= RB and fewer than NB
+// columns are in flight.  All positions are 32-bit, no modulo arithmetic.
 #include "pam_common.cuh"
 
 #include <stdlib.h>
@@ -118,9 +118,10 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tiles_kernel(const CdTilesArgs
           }
           const unsigned mk = __shfl_sync(0xffffffffu, iss_mask_l, p_col & 31);
           const int nd = 32 * __popc(mk);
-          const int waste = (p_phys + nd > RB) ? RB - p_phys : 0;
+          const bool wrap = p_phys + nd > RB;  // (p_phys == RB wraps even with zero waste)
+          const int waste = wrap ? RB - p_phys : 0;
           if (in_use + waste + nd > RB) break;  // ring full until the consumer releases
-          const int start = waste ? 0 : p_phys;
+          const int start = wrap ? 0 : p_phys;
           const int off = __shfl_sync(0xffffffffu, iss_off_l, p_col & 31);
           if (lane == 0) {
             uint64_t* bar = &bars[seq_issue & (NB - 1)];
@@ -142,8 +143,9 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tiles_kernel(const CdTilesArgs
       int cur_nd = 0, cur_free = 0;
       auto acquire = [&](unsigned mk) -> const double* {
         cur_nd = 32 * __popc(mk);
-        const int waste = (c_phys + cur_nd > RB) ? RB - c_phys : 0;
-        const int start = waste ? 0 : c_phys;
+        const bool wrap = c_phys + cur_nd > RB;
+        const int waste = wrap ? RB - c_phys : 0;
+        const int start = wrap ? 0 : c_phys;
         cur_free = waste + cur_nd;
         c_phys = start + cur_nd;
         mbar_wait(&bars[seq_cons & (NB - 1)], (seq_cons / NB) & 1u);
