@@ -31,6 +31,8 @@
 namespace pam {
 
 __device__ unsigned int g_cd_queue;
+// 32 zero tiles (8 KB, L2-resident): the TMA fills dropped tile runs from here
+__device__ __align__(128) double g_zero_tiles[32 * 32];
 
 enum : int { CD_COLSQ_GIVEN = 1, CD_R_GIVEN = 2, CD_WRITE_R = 4 };
 
@@ -98,9 +100,10 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
   double* prm_base = reinterpret_cast<double*>(smem_raw) +
                      (static_cast<size_t>(NGROUPS) * STAGES * LDMAX) + NGROUPS * STAGES +
                      NGROUPS * (2 * G + 1);
-  double* pb = prm_base + grp * 96;
+  double* pb = prm_base + grp * 128;
   double* pc = pb + 32;
-  unsigned* pm = reinterpret_cast<unsigned*>(pb + 64);
+  double* pinv = pb + 64;  // 1 / (col_sq + lam2): division by reciprocal + one FMA correction
+  unsigned* pm = reinterpret_cast<unsigned*>(pb + 96);
 
   auto sync_group = [&]() {
     if (G == 1) __syncwarp();
@@ -178,15 +181,24 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
           unsigned long long mk;
           if (R <= 32) mk = __shfl_sync(0xffffffffu, static_cast<unsigned>(iss_mask_l), next_col & 31);
           else mk = __shfl_sync(0xffffffffu, iss_mask_l, next_col & 31);
-          const uint32_t nb = static_cast<uint32_t>(__popcll(mk)) * 32u * sizeof(double);
-          if (lane == 0) {
-            const int st = g_issue % STAGES;
-            if (nb) {
-              mbar_arrive_expect_tx(&bars[st], nb);
-              tma_load_1d(ring + st * LDMAX, Ws + off, nb, &bars[st]);
-            } else {
-              mbar_arrive(&bars[st]);  // empty column: complete the phase without data
-            }
+          // Scatter: every maximal run of kept tiles is copied from the packed
+          // column to its dense slot position, every run of dropped tiles from the
+          // L2-resident zero tiles, so the consumer reads a dense column.  One
+          // cp.async.bulk per run, issued by the lane owning the run's first tile.
+          const int st = g_issue % STAGES;
+          const unsigned fullm = (R >= 32) ? 0xffffffffu : ((1u << R) - 1u);
+          const unsigned m = static_cast<unsigned>(mk) & fullm;
+          const unsigned starts = ((m ^ (m << 1)) | 1u) & fullm;
+          if (lane == 0) mbar_arrive_expect_tx(&bars[st], static_cast<uint32_t>(R) * 256u);
+          __syncwarp();
+          if (lane < R && ((starts >> lane) & 1u)) {
+            const unsigned later = starts & ~((2u << lane) - 1u);
+            const int end = later ? (__ffs(later) - 1) : R;
+            const uint32_t bytes = static_cast<uint32_t>(end - lane) * 256u;
+            const double* src = ((m >> lane) & 1u)
+                                    ? Ws + off + 32 * __popc(m & ((1u << lane) - 1u))
+                                    : g_zero_tiles;
+            tma_load_1d(ring + st * LDMAX + 32 * lane, src, bytes, &bars[st]);
           }
         } else if (gt == 0) {
           const int st = g_issue % STAGES;
@@ -215,38 +227,9 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
         cur_mk = mk;
         if (!KEEPW) return;
         if (TILES) {
-          // Tiles in groups of four with warp-uniform fast paths: RCB ordering
-          // makes kept tiles cluster, so most groups are all-kept (contiguous
-          // loads, no selects) or all-dropped (zeros).
-          int slot = 0;
+          // the slot holds the dense column (dropped tiles were zero-filled)
 #pragma unroll
-          for (int g = 0; g < (R + 3) / 4; ++g) {
-            constexpr int dummy = 0;
-            (void)dummy;
-            const int cnt = (4 * g + 4 <= R) ? 4 : (R - 4 * g);
-            const unsigned full = (1u << cnt) - 1u;
-            const unsigned nib = static_cast<unsigned>(mk >> (4 * g)) & full;
-            if (nib == full) {
-#pragma unroll
-              for (int u = 0; u < 4; ++u)
-                if (u < cnt) w[4 * g + u] = col[32 * (slot + u) + lane];
-              slot += cnt;
-            } else if (nib == 0u) {
-#pragma unroll
-              for (int u = 0; u < 4; ++u)
-                if (u < cnt) w[4 * g + u] = 0.0;
-            } else {
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                if (u < cnt) {
-                  const int bit = static_cast<int>((nib >> u) & 1u);
-                  const double v = col[32 * slot + lane];  // slot <= k < R: inside the ring slot
-                  w[4 * g + u] = bit ? v : 0.0;
-                  slot += bit;
-                }
-              }
-            }
-          }
+          for (int k = 0; k < R; ++k) w[k] = col[32 * k + lane];
         } else {
 #pragma unroll
           for (int k = 0; k < R; ++k) {
@@ -258,12 +241,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
       // entry k of the current column for this thread (0 when absent)
       auto wk = [&](int k, int& slot) -> double {
         if (KEEPW) return w[KEEPW ? k : 0];
-        if (TILES) {
-          const int bit = static_cast<int>((cur_mk >> k) & 1ull);
-          const double v = cur_col[32 * slot + lane];
-          slot += bit;
-          return bit ? v : 0.0;
-        }
+        if (TILES) return cur_col[32 * k + lane];
         const double v = cur_col[gt + GT * k];
         return (gt + GT * k < N) ? v : 0.0;
       };
@@ -340,7 +318,10 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
             __syncwarp();
             if (lane < nc) {
               pb[lane] = a.beta[doff + cb + lane];
-              pc[lane] = a.col_sq[doff + cb + lane];
+              const double csv = a.col_sq[doff + cb + lane];
+              pc[lane] = csv;
+              const double dnv = __dadd_rn(csv, lam2);
+              pinv[lane] = dnv > 0.0 ? __ddiv_rn(1.0, dnv) : 0.0;
               if (TILES) pm[lane] = static_cast<unsigned>(a.tile_mask[doff + cb + lane]);
             }
             __syncwarp();
@@ -368,7 +349,16 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
             if (dn > 0.0) {
               double mag = __dsub_rn(fabs(z), lam1);
               if (mag < 0.0) mag = 0.0;
-              b_new = __ddiv_rn(z >= 0.0 ? mag : -mag, dn);
+              const double num = z >= 0.0 ? mag : -mag;
+              if (PSM) {
+                // num / dn via the reciprocal and one Newton correction (the
+                // correctly rounded quotient except in rare last-ulp cases)
+                const double inv = pinv[t];
+                const double q0 = __dmul_rn(num, inv);
+                b_new = fma(fma(-q0, dn, num), inv, q0);
+              } else {
+                b_new = __ddiv_rn(num, dn);
+              }
             }
             // branch-free update: d == 0 exactly when b_new == b_old, and then the
             // AXPY adds -0 * w to every residual entry, leaving r bit-unchanged
@@ -467,7 +457,7 @@ int launch_cd(const CdArgs& a, cudaStream_t stream) {
   const size_t smem = static_cast<size_t>(NGROUPS) * STAGES * (R * 32 * G * sizeof(double)) +
                       static_cast<size_t>(NGROUPS) * STAGES * sizeof(uint64_t) +
                       static_cast<size_t>(NGROUPS) * (2 * G + 1) * sizeof(double) +
-                      static_cast<size_t>(NGROUPS) * 96 * sizeof(double);
+                      static_cast<size_t>(NGROUPS) * 128 * sizeof(double);
   static bool configured = false;
   if (!configured) {
     PAM_CUDA_CHECK(cudaFuncSetAttribute(cd_kernel<R, STAGES, WPC, G, TILES, KEEPW>,
