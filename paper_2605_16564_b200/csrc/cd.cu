@@ -31,8 +31,6 @@
 namespace pam {
 
 __device__ unsigned int g_cd_queue;
-// 32 zero tiles (8 KB, L2-resident): the TMA fills dropped tile runs from here
-__device__ __align__(128) double g_zero_tiles[32 * 32];
 
 enum : int { CD_COLSQ_GIVEN = 1, CD_R_GIVEN = 2, CD_WRITE_R = 4 };
 
@@ -72,8 +70,9 @@ __device__ __forceinline__ void group_bar(int id, int nthreads) {
 
 // R: rows per thread, STAGES: ring depth, WPC: warps per CTA, G: warps per
 // subdomain group (rows of a subdomain split over the G*32 threads).
-template <int R, int STAGES, int WPC, int G, bool TILES, bool KEEPW = true>
+template <int R, int STAGES, int WPC, int G, bool TILES, bool KEEPW = true, bool LDGSTS = false>
 __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
+  static_assert(!LDGSTS || (G == 1 && STAGES == 3), "LDGSTS staging: one warp, 3 stages");
   static_assert(!TILES || G == 1, "tile-packed columns are consumed one warp per subdomain");
   constexpr int GT = G * 32;         // threads per group
   constexpr int LDMAX = R * GT;      // rows per ring slot
@@ -181,24 +180,22 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
           unsigned long long mk;
           if (R <= 32) mk = __shfl_sync(0xffffffffu, static_cast<unsigned>(iss_mask_l), next_col & 31);
           else mk = __shfl_sync(0xffffffffu, iss_mask_l, next_col & 31);
-          // Scatter: every maximal run of kept tiles is copied from the packed
-          // column to its dense slot position, every run of dropped tiles from the
-          // L2-resident zero tiles, so the consumer reads a dense column.  One
-          // cp.async.bulk per run, issued by the lane owning the run's first tile.
-          const int st = g_issue % STAGES;
-          const unsigned fullm = (R >= 32) ? 0xffffffffu : ((1u << R) - 1u);
-          const unsigned m = static_cast<unsigned>(mk) & fullm;
-          const unsigned starts = ((m ^ (m << 1)) | 1u) & fullm;
-          if (lane == 0) mbar_arrive_expect_tx(&bars[st], static_cast<uint32_t>(R) * 256u);
-          __syncwarp();
-          if (lane < R && ((starts >> lane) & 1u)) {
-            const unsigned later = starts & ~((2u << lane) - 1u);
-            const int end = later ? (__ffs(later) - 1) : R;
-            const uint32_t bytes = static_cast<uint32_t>(end - lane) * 256u;
-            const double* src = ((m >> lane) & 1u)
-                                    ? Ws + off + 32 * __popc(m & ((1u << lane) - 1u))
-                                    : g_zero_tiles;
-            tma_load_1d(ring + st * LDMAX + 32 * lane, src, bytes, &bars[st]);
+          const uint32_t nb = static_cast<uint32_t>(__popcll(mk)) * 32u * sizeof(double);
+          if (LDGSTS) {
+            // per-lane 16-byte async copies of the packed column (no TMA unit)
+            double* dst = ring + (g_issue % STAGES) * LDMAX;
+            const double* src = Ws + off;
+            const int pieces = static_cast<int>(nb / 16u);
+            for (int i = lane; i < pieces; i += 32) cp_async16(dst + 2 * i, src + 2 * i);
+            cp_async_commit();
+          } else if (lane == 0) {
+            const int st = g_issue % STAGES;
+            if (nb) {
+              mbar_arrive_expect_tx(&bars[st], nb);
+              tma_load_1d(ring + st * LDMAX, Ws + off, nb, &bars[st]);
+            } else {
+              mbar_arrive(&bars[st]);  // empty column: complete the phase without data
+            }
           }
         } else if (gt == 0) {
           const int st = g_issue % STAGES;
@@ -211,7 +208,15 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
       };
       auto wait_one = [&]() -> const double* {
         const int st = g_cons % STAGES;
-        mbar_wait(&bars[st], (g_cons / STAGES) & 1u);
+        if (LDGSTS) {
+          const int ahead = static_cast<int>(g_issue - g_cons) - 1;  // groups that may stay in flight
+          if (ahead >= 2) cp_async_wait<2>();
+          else if (ahead == 1) cp_async_wait<1>();
+          else cp_async_wait<0>();
+          __syncwarp();
+        } else {
+          mbar_wait(&bars[st], (g_cons / STAGES) & 1u);
+        }
         ++g_cons;
         return ring + st * LDMAX;
       };
@@ -227,9 +232,38 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
         cur_mk = mk;
         if (!KEEPW) return;
         if (TILES) {
-          // the slot holds the dense column (dropped tiles were zero-filled)
+          // Tiles in groups of four with warp-uniform fast paths: RCB ordering
+          // makes kept tiles cluster, so most groups are all-kept (contiguous
+          // loads, no selects) or all-dropped (zeros).
+          int slot = 0;
 #pragma unroll
-          for (int k = 0; k < R; ++k) w[k] = col[32 * k + lane];
+          for (int g = 0; g < (R + 3) / 4; ++g) {
+            constexpr int dummy = 0;
+            (void)dummy;
+            const int cnt = (4 * g + 4 <= R) ? 4 : (R - 4 * g);
+            const unsigned full = (1u << cnt) - 1u;
+            const unsigned nib = static_cast<unsigned>(mk >> (4 * g)) & full;
+            if (nib == full) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (u < cnt) w[4 * g + u] = col[32 * (slot + u) + lane];
+              slot += cnt;
+            } else if (nib == 0u) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (u < cnt) w[4 * g + u] = 0.0;
+            } else {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                if (u < cnt) {
+                  const int bit = static_cast<int>((nib >> u) & 1u);
+                  const double v = col[32 * slot + lane];  // slot <= k < R: inside the ring slot
+                  w[4 * g + u] = bit ? v : 0.0;
+                  slot += bit;
+                }
+              }
+            }
+          }
         } else {
 #pragma unroll
           for (int k = 0; k < R; ++k) {
@@ -241,7 +275,12 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
       // entry k of the current column for this thread (0 when absent)
       auto wk = [&](int k, int& slot) -> double {
         if (KEEPW) return w[KEEPW ? k : 0];
-        if (TILES) return cur_col[32 * k + lane];
+        if (TILES) {
+          const int bit = static_cast<int>((cur_mk >> k) & 1ull);
+          const double v = cur_col[32 * slot + lane];
+          slot += bit;
+          return bit ? v : 0.0;
+        }
         const double v = cur_col[gt + GT * k];
         return (gt + GT * k < N) ? v : 0.0;
       };
@@ -419,6 +458,12 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
                         __dmul_rn(__dmul_rn(0.5, lam2), l2));
       }
       // drain speculative prefetches of the sweep that will not run
+      if (LDGSTS) {
+        cp_async_wait<0>();
+        __syncwarp();
+        g_cons += static_cast<uint32_t>(issued - consumed);
+        consumed = issued;
+      }
       while (consumed < issued) {
         (void)wait_one();
         ++consumed;
@@ -451,7 +496,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
   }
 }
 
-template <int R, int STAGES, int WPC, int G, bool TILES = false, bool KEEPW = true>
+template <int R, int STAGES, int WPC, int G, bool TILES = false, bool KEEPW = true, bool LDGSTS = false>
 int launch_cd(const CdArgs& a, cudaStream_t stream) {
   constexpr int NGROUPS = WPC / G;
   const size_t smem = static_cast<size_t>(NGROUPS) * STAGES * (R * 32 * G * sizeof(double)) +
@@ -460,7 +505,7 @@ int launch_cd(const CdArgs& a, cudaStream_t stream) {
                       static_cast<size_t>(NGROUPS) * 128 * sizeof(double);
   static bool configured = false;
   if (!configured) {
-    PAM_CUDA_CHECK(cudaFuncSetAttribute(cd_kernel<R, STAGES, WPC, G, TILES, KEEPW>,
+    PAM_CUDA_CHECK(cudaFuncSetAttribute(cd_kernel<R, STAGES, WPC, G, TILES, KEEPW, LDGSTS>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
@@ -471,7 +516,7 @@ int launch_cd(const CdArgs& a, cudaStream_t stream) {
   PAM_CUDA_CHECK(cudaGetSymbolAddress(&qaddr, g_cd_queue));
   PAM_CUDA_CHECK(cudaMemsetAsync(qaddr, 0, sizeof(unsigned), stream));
   const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(sms, a.S));
-  cd_kernel<R, STAGES, WPC, G, TILES, KEEPW><<<(unsigned)ctas, WPC * 32, smem, stream>>>(a);
+  cd_kernel<R, STAGES, WPC, G, TILES, KEEPW, LDGSTS><<<(unsigned)ctas, WPC * 32, smem, stream>>>(a);
   PAM_LAUNCH_CHECK("cd_kernel");
   return PAM_OK;
 }
@@ -511,6 +556,8 @@ int cd_dispatch_tiles(const CdArgs& a, int max_rows, cudaStream_t stream) {
   if (max_rows <= 512) {
     static const char* env = getenv("PAM_CD_WPC16");
     const int v = env ? atoi(env) : 16;
+    static const char* cp = getenv("PAM_CD_COPY");
+    if (cp && cp[0] == 'l') return launch_cd<16, 3, 16, 1, true, true, true>(a, stream);
     if (v == 24) return launch_cd<16, 2, 24, 1, true, false>(a, stream);
     if (v == 20) return launch_cd<16, 2, 20, 1, true, false>(a, stream);
     return launch_cd<16, 3, 16, 1, true>(a, stream);
