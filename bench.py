@@ -251,8 +251,22 @@ def run_ours(args):
             record.append((rep, e0, e1))
         return sur, rep
 
+    warm = None
     for _ in range(args.warmup):
-        step()
+        warm = step()
+    if warm is None:
+        warm = step()
+    # evaluation work: point-centre pairs = sum over points of the owner's M
+    m_sizes = np.array([len(l.dictionary) for l in warm[0].locals], dtype=np.int64)
+    _, edges = part.grid
+    own = np.zeros(P, dtype=np.int64)
+    stride = 1
+    for k in range(3):
+        idx = np.clip(np.searchsorted(edges[k], wl.eval_points[:, k], side="right") - 1, 0, part.shape[k] - 1)
+        own += stride * idx
+        stride *= part.shape[k]
+    eval_pairs = int(m_sizes[own].sum())
+    fp64_peak = nat.measure_fp64_peak()
     barrier()
     lib = nat.lib()
     lib.reset_counters()
@@ -273,6 +287,7 @@ def run_ours(args):
     cd_s = sum(r.device["kernel_seconds"]["cd"] for r, _, _ in recs)
     cd_bytes = sum(r.device["cd_bytes"] for r, _, _ in recs)
     cd_flops = sum(r.device["cd_flops"] for r, _, _ in recs)
+    cd_dense = sum(r.device.get("cd_dense_bytes", 0) for r, _, _ in recs)
     cd_launches = sum(r.device["cd_launches"] for r, _, _ in recs)
     kt = {}
     for r, _, _ in recs:
@@ -359,7 +374,17 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": cd_bytes / max(cd_launches, 1),
                      "avg_launch_s": cd_s / max(cd_launches, 1),
                      "fp64_gflops": cd_flops / cd_s / 1e9 if cd_s > 0 else 0.0,
-                     "step_share": cd_s / (elapsed * (1 if world == 1 else 1)) if elapsed else None},
+                     "dense_equivalent_bytes_per_launch": cd_dense / max(cd_launches, 1),
+                     "tile_tau": __import__("paper_2605_16564_b200.engine", fromlist=["x"]).tile_tau(),
+                     "step_share": cd_s / elapsed if elapsed else None},
+        "eval_roofline": {"kernel": "eval_kernel (locate + owner sort + two-pass Shepard + exp)",
+                          "bound": "fp64", "unit": "GFLOP/s",
+                          "flops_per_pair": 3 * 3 + 4 + 20,
+                          "flop_convention": "SURVEY 8d: M_owner*(3d+4+E) per point, E=20 FP64 ops per exp",
+                          "pairs_per_step": eval_pairs,
+                          "achieved": eval_pairs * 33 / (eval_s / args.steps) / 1e9,
+                          "peak": fp64_peak / 1e9, "peak_source": "measured (pam_probe_fp64, FMA=2)",
+                          "frac": eval_pairs * 33 / (eval_s / args.steps) / fp64_peak},
         "kernel_seconds_per_step": {k: v / args.steps for k, v in kt.items()},
         "gpu_launches": launches,
         "clocks": clocks,

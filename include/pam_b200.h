@@ -249,6 +249,11 @@ int pam_shepard_eval_f64(int dim, int64_t P, const double* pts, int64_t M,
                          const double* beta, int32_t exp_out, double* out,
                          int64_t* err, void* stream);
 
+/* FP64 pipe probe: launches 4*SMs x 256 threads, each running 8 independent
+ * DFMA chains of `iters` steps (2 flops per DFMA); the caller times it to get
+ * the measured FP64 peak (roofline denominator for the FP64-bound kernels). */
+int pam_probe_fp64(int64_t iters, double* out, void* stream);
+
 /* ---- host-pointer synchronous seams (drop-in for the reference) ---------- */
 
 /* Exact signature of _cd_sweeps_jit (elastic_net.py:113): W is the (n, m)

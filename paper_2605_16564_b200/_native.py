@@ -104,6 +104,7 @@ SIGNATURES = {
         ctypes.c_int,
         [ctypes.c_int, _ptr, _ptr, _ptr, _ptr, _ptr, _i64, _ptr, _ptr, _ptr, _ptr, _ptr],
     ),
+    "pam_probe_fp64": (ctypes.c_int, [_i64, _ptr, _ptr]),
     "pam_cd_sweeps_host_f64": (
         ctypes.c_int,
         [_ptr, _i64, _i64, _ptr, _ptr, _dbl, _dbl, _dbl, _i64, _ptr, _ptr, _ptr, _ptr, _ptr],
@@ -161,7 +162,7 @@ class _CountingLib:
         "pam_cd_ex_f64": 1, "pam_residual_f64": 2, "pam_mark_f64": 1, "pam_enrich_f64": 1,
         "pam_locate_f64": 1, "pam_eval_f64": 5, "pam_shepard_eval_f64": 1,
         "pam_row_normalize_f64": 1, "pam_gather_cells_f64": 1, "pam_assemble_tiles_f64": 3,
-        "pam_cd_tiles_f64": 1, "pam_gram_f64": 2, "pam_cd_gram_f64": 1,
+        "pam_cd_tiles_f64": 1, "pam_gram_f64": 2, "pam_cd_gram_f64": 1, "pam_probe_fp64": 1,
     }
 
     def __init__(self, raw):
@@ -287,6 +288,22 @@ def raise_data_error(code: int, index: int, context: str = ""):
     if code == PAM_ERR_UNSUPPORTED:
         raise NumericalError(f"dictionary capacity exceeded in subdomain {index}")
     raise RuntimeError(f"device error {code} at index {index}")
+
+
+def measure_fp64_peak(iters: int = 200_000) -> float:
+    """Measured FP64 peak (flop/s, FMA = 2) of this GPU via pam_probe_fp64."""
+    torch = torch_mod()
+    dev = device()
+    out = torch.zeros(1, dtype=torch.float64, device=dev)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    check(lib().pam_probe_fp64(1000, ptr(out), stream_ptr()), "pam_probe_fp64")  # warm-up
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    check(lib().pam_probe_fp64(iters, ptr(out), stream_ptr()), "pam_probe_fp64")
+    e1.record()
+    e1.synchronize()
+    sec = e0.elapsed_time(e1) / 1e3
+    return sms * 4 * 256 * 8 * iters * 2.0 / sec
 
 
 def available() -> bool:

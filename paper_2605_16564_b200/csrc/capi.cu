@@ -139,3 +139,32 @@ extern "C" int pam_shepard_eval_host_f64(int dim, int64_t P, const double* pts, 
   }
   return PAM_OK;
 }
+
+// ---- FP64 pipe probe: the measured DFMA peak used as the FP64 roofline
+// denominator (MEASURED_PEAKS.json carries HBM and bf16 only).  Each thread
+// runs 8 independent DFMA chains; grid = 4 x SMs, 256 threads.
+namespace pam {
+__global__ void __launch_bounds__(256) fp64_probe_kernel(int64_t iters, double* out) {
+  double a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = 1.0 + 1e-9 * (threadIdx.x + k);
+  const double m = 0.9999999999, c = 1e-10;
+  for (int64_t i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fma(a[k], m, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.0) out[0] = s;  // keep the work alive
+}
+}  // namespace pam
+
+extern "C" int pam_probe_fp64(int64_t iters, double* out, void* stream) {
+  int dev = 0, sms = 148;
+  PAM_CUDA_CHECK(cudaGetDevice(&dev));
+  PAM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  pam::fp64_probe_kernel<<<sms * 4, 256, 0, as_stream(stream)>>>(iters, out);
+  PAM_LAUNCH_CHECK("fp64_probe_kernel");
+  return PAM_OK;
+}

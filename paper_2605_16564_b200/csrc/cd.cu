@@ -554,9 +554,9 @@ int cd_dispatch_tiles(const CdArgs& a, int max_rows, cudaStream_t stream) {
   if (max_rows <= 128) return launch_cd<4, 4, 16, 1, true>(a, stream);
   if (max_rows <= 256) return launch_cd<8, 4, 16, 1, true>(a, stream);
   if (max_rows <= 512) {
-    static const char* env = getenv("PAM_CD_WPC16");
+    const char* env = getenv("PAM_CD_WPC16");
     const int v = env ? atoi(env) : 16;
-    static const char* cp = getenv("PAM_CD_COPY");
+    const char* cp = getenv("PAM_CD_COPY");
     if (cp && cp[0] == 'l') return launch_cd<16, 3, 16, 1, true, true, true>(a, stream);
     if (v == 24) return launch_cd<16, 2, 24, 1, true, false>(a, stream);
     if (v == 20) return launch_cd<16, 2, 20, 1, true, false>(a, stream);
@@ -608,7 +608,7 @@ extern "C" int pam_cd_tiles_f64(int64_t S, const int64_t* order, const int64_t* 
                                 void* stream) {
   if (S < 0 || max_rows < 0 || !tile_mask || !col_off) return PAM_ERR_ARG;
   if (S == 0) return PAM_OK;
-  static const char* ring_env = getenv("PAM_CD_RING");
+  const char* ring_env = getenv("PAM_CD_RING");
   if (hist == nullptr && max_rows <= 1024 && ring_env && atoi(ring_env) == 1)
     return pam_cd_tiles_ring(S, order, row_off, y, perm, dict_off, m_cur, w_off, tile_mask, col_off,
                              W, lam1, lam2, tol, max_iters, active, max_rows, beta, col_sq, sweeps,

@@ -338,7 +338,7 @@ int pam_cd_tiles_ring(int64_t S, const int64_t* order, const int64_t* row_off, c
                 max_iters, active, beta, col_sq, sweeps, converged, objective};
   cudaStream_t st = as_stream(stream);
   // ring sized so WPC * RB doubles ~ 200 KB per SM; NB mbarriers per warp
-  static const char* env = getenv("PAM_RING_WPC");
+  const char* env = getenv("PAM_RING_WPC");
   const int wpc = env ? atoi(env) : 16;
   if (max_rows <= 128) return launch_cd_tiles<4, 16, 1536, 16>(a, st);
   if (max_rows <= 256) return launch_cd_tiles<8, 16, 1536, 16>(a, st);

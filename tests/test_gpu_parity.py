@@ -234,6 +234,23 @@ def test_tile_packed_stream_matches_dense(cuda, monkeypatch, cells):
             assert abs(x.rel_l2 - y.rel_l2) <= 1e-10 * x.rel_l2
 
 
+@pytest.mark.parametrize("variant", [{"PAM_CD_RING": "1"}, {"PAM_CD_COPY": "ldgsts"}])
+def test_cd_staging_variants_match(cuda, monkeypatch, variant):
+    """Opt-in CD staging variants (byte ring, LDGSTS) reproduce the default kernel."""
+    field = pam.box_field_2d(40, 40)
+    part = pam.make_partition(field.mesh, 2, 2)  # 400 rows: the R=16 tile kernels
+    cfg = pam.AdaptiveConfig(k_top=40, m_max=240, m_q=3, max_rounds=3, elastic=EN_2D,
+                             offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
+    spec = pam.DictionarySpec(sigma=0.5 / 40)
+    base, rb = pam.fit_parallel(field, part, cfg, spec)
+    for k, v in variant.items():
+        monkeypatch.setenv(k, v)
+    other, ro = pam.fit_parallel(field, part, cfg, spec)
+    for a, b in zip(base.locals, other.locals):
+        np.testing.assert_array_equal(a.dictionary.centers, b.dictionary.centers)
+        assert np.max(np.abs(a.beta - b.beta)) <= 1e-10 * max(1, np.abs(a.beta).max())
+
+
 def test_gram_form_matches_residual_form(cuda, monkeypatch):
     """Covariance-form CD (gram.cu) vs residual form on a lattice dictionary with refinement."""
     field = pam.box_field_2d(32, 32)
