@@ -419,7 +419,9 @@ def run_c5(args):
     layers = args.c5_layers
     n_sub = 64 * 32 * layers
     n_eval = int(1e8 * layers / 32)
-    p = workloads.config5(M=args.m, n_sub=n_sub, n_eval=n_eval)
+    p = workloads.config5(M=args.m, n_sub=n_sub, n_eval=0)
+    # 1e8 uniform points over the full 64x32x32 domain, restricted to the fitted slab
+    p.eval_points = np.random.default_rng(50).random((n_eval, 3)) * np.array([64.0, 32.0, float(layers)])
     dev = nat.device()
     d_pts = torch.from_numpy(p.points.reshape(-1)).to(dev)
     d_vals = torch.from_numpy(p.values).to(dev)

@@ -271,6 +271,12 @@ int pam_shepard_eval_host_f64(int dim, int64_t P, const double* pts, int64_t M,
                               const double* centres, const double* widths,
                               const double* beta, double* out, int64_t* err_index);
 
+/* Surrogate text format fast path (partition.py:220-247 `save`): n entry
+ * lines "<centre coords> <width> <beta> <generation>\n", reals as %.17g.
+ * Returns bytes written into out[cap], or -1 when cap is too small. */
+int64_t pam_format_entries_host(int dim, int64_t n, const double* centres, const double* widths,
+                                const double* beta, const int64_t* gens, char* out, int64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -105,6 +105,7 @@ SIGNATURES = {
         [ctypes.c_int, _ptr, _ptr, _ptr, _ptr, _ptr, _i64, _ptr, _ptr, _ptr, _ptr, _ptr],
     ),
     "pam_probe_fp64": (ctypes.c_int, [_i64, _ptr, _ptr]),
+    "pam_format_entries_host": (_i64, [ctypes.c_int, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _i64]),
     "pam_cd_sweeps_host_f64": (
         ctypes.c_int,
         [_ptr, _i64, _i64, _ptr, _ptr, _dbl, _dbl, _dbl, _i64, _ptr, _ptr, _ptr, _ptr, _ptr],

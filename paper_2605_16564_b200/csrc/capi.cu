@@ -168,3 +168,29 @@ extern "C" int pam_probe_fp64(int64_t iters, double* out, void* stream) {
   PAM_LAUNCH_CHECK("fp64_probe_kernel");
   return PAM_OK;
 }
+
+// ---- surrogate text format fast path (reference partition.py:220-247) ------
+// Formats n dictionary entries as "<c_0> ... <c_dim-1> <width> <beta> <gen>\n"
+// with %.17g for reals (glibc printf is correctly rounded, identical to
+// Python's format(v, '.17g')).  Returns bytes written, or -1 if `cap` is too
+// small.  Host-only; no GPU needed.
+extern "C" int64_t pam_format_entries_host(int dim, int64_t n, const double* centres,
+                                           const double* widths, const double* beta,
+                                           const int64_t* gens, char* out, int64_t cap) {
+  int64_t pos = 0;
+  char buf[64];
+  for (int64_t i = 0; i < n; ++i) {
+    for (int k = 0; k < dim + 3; ++k) {
+      int len;
+      if (k < dim) len = snprintf(buf, sizeof(buf), "%.17g", centres[i * dim + k]);
+      else if (k == dim) len = snprintf(buf, sizeof(buf), "%.17g", widths[i]);
+      else if (k == dim + 1) len = snprintf(buf, sizeof(buf), "%.17g", beta[i]);
+      else len = snprintf(buf, sizeof(buf), "%lld", static_cast<long long>(gens[i]));
+      if (pos + len + 1 > cap) return -1;
+      memcpy(out + pos, buf, len);
+      pos += len;
+      out[pos++] = (k == dim + 2) ? '\n' : ' ';
+    }
+  }
+  return pos;
+}

@@ -214,7 +214,33 @@ def geometry_case():
     print("  geometry.npz written")
 
 
+def persistence_case():
+    """Reference `dumps` text of a surrogate with awkward values (-0.0, denormals, 1e+/-300)."""
+    from fieldfit.partition import dumps as r_dumps, make_partition as r_part
+    from fieldfit.geometry import build_mesh as r_mesh
+
+    rng = np.random.default_rng(99)
+    part = r_part(r_mesh(2, (8, 6), ((0.0, 1.0), (-2.0, 1.0))), 2, 3)
+    out, locs = {}, []
+    for i, b in enumerate(part.boxes):
+        n = 5 + i
+        c = np.asarray(b.lo) + rng.random((n, 2)) * (np.asarray(b.hi) - np.asarray(b.lo))
+        w = rng.uniform(1e-5, 0.3, n)
+        be = rng.standard_normal(n) * 10.0 ** rng.integers(-300, 300, n)
+        be[0], be[1] = -0.0, 5e-324
+        g = rng.integers(0, 5, n)
+        out[f"c{i}"], out[f"w{i}"], out[f"b{i}"], out[f"g{i}"] = c, w, be, g
+        locs.append(ff.LocalSurrogate(dictionary=RDict(centers=c, widths=w, generations=g), beta=be))
+    text = r_dumps(ff.GlobalSurrogate(partition=part, locals=tuple(locs),
+                                      metadata={"config": "golden persistence", "field_checksum": "abc"}))
+    np.savez_compressed(OUT / "persistence.npz", **out)
+    (OUT / "surrogate_ref.txt").write_text(text)
+    print("  persistence fixtures written")
+
+
 def main(which):
+    if "persistence" in which:
+        persistence_case()
     if "geometry" in which:
         geometry_case()
     if "kernels" in which:

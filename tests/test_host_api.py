@@ -172,3 +172,23 @@ def test_workload_shapes():
     assert np.all(p.points >= np.repeat(p.box_lo, 1000, axis=0))
     assert np.all(p.points < np.repeat(p.box_hi, 1000, axis=0))
     assert np.all(p.values > 0)
+
+
+def test_save_byte_identical_to_reference_writer(golden):
+    """dumps() reproduces the reference's text (partition.py:224-247) byte for byte."""
+    from pathlib import Path
+
+    g = golden("persistence")
+    part = pam.make_partition(pam.build_mesh(2, (8, 6), ((0.0, 1.0), (-2.0, 1.0))), 2, 3)
+    locs = tuple(
+        pam.LocalSurrogate(dictionary=pam.RbfDictionary(centers=g[f"c{i}"], widths=g[f"w{i}"],
+                                                        generations=g[f"g{i}"]), beta=g[f"b{i}"])
+        for i in range(6))
+    sur = pam.GlobalSurrogate(partition=part, locals=locs,
+                              metadata={"config": "golden persistence", "field_checksum": "abc"})
+    ref = (Path(__file__).parent / "golden" / "surrogate_ref.txt").read_text()
+    assert pam.dumps(sur) == ref
+    back = pam.loads(ref)
+    assert pam.dumps(back) == ref
+    for a, b in zip(back.locals, locs):
+        np.testing.assert_array_equal(a.beta, b.beta)
