@@ -232,37 +232,15 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
         cur_mk = mk;
         if (!KEEPW) return;
         if (TILES) {
-          // Tiles in groups of four with warp-uniform fast paths: RCB ordering
-          // makes kept tiles cluster, so most groups are all-kept (contiguous
-          // loads, no selects) or all-dropped (zeros).
-          int slot = 0;
+          // tile masks are contiguous ranges [k0, k0 + len) (tiles.cu): tile k
+          // sits at slot k - k0 of the staged column, tiles outside are zero
+          const int k0 = mk ? (__ffsll(static_cast<long long>(mk)) - 1) : 0;
+          const unsigned len = static_cast<unsigned>(__popcll(mk));
+          const double* base = col - 32 * k0 + lane;
 #pragma unroll
-          for (int g = 0; g < (R + 3) / 4; ++g) {
-            constexpr int dummy = 0;
-            (void)dummy;
-            const int cnt = (4 * g + 4 <= R) ? 4 : (R - 4 * g);
-            const unsigned full = (1u << cnt) - 1u;
-            const unsigned nib = static_cast<unsigned>(mk >> (4 * g)) & full;
-            if (nib == full) {
-#pragma unroll
-              for (int u = 0; u < 4; ++u)
-                if (u < cnt) w[4 * g + u] = col[32 * (slot + u) + lane];
-              slot += cnt;
-            } else if (nib == 0u) {
-#pragma unroll
-              for (int u = 0; u < 4; ++u)
-                if (u < cnt) w[4 * g + u] = 0.0;
-            } else {
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                if (u < cnt) {
-                  const int bit = static_cast<int>((nib >> u) & 1u);
-                  const double v = col[32 * slot + lane];  // slot <= k < R: inside the ring slot
-                  w[4 * g + u] = bit ? v : 0.0;
-                  slot += bit;
-                }
-              }
-            }
+          for (int k = 0; k < R; ++k) {
+            const bool in = static_cast<unsigned>(k - k0) < len;
+            w[k] = in ? base[32 * k] : 0.0;
           }
         } else {
 #pragma unroll

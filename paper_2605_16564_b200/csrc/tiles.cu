@@ -127,6 +127,19 @@ __global__ void __launch_bounds__(SC_THREADS) tile_scan_kernel(const TileArgs a)
   const int64_t doff = a.dict_off[s];
   const int per = (M + SC_THREADS - 1) / SC_THREADS;
   const int lo = threadIdx.x * per, hi = min(M, lo + per);
+  // Range form: keep every tile between a column's first and last kept tile
+  // (interior tiles are stored with their exact small values), so the CD
+  // kernel addresses a column as one contiguous run: +~12% bytes at C4 but a
+  // single predicated load per tile instead of per-tile slot arithmetic.
+  for (int j = lo; j < hi; ++j) {
+    const unsigned long long m = a.tile_mask[doff + j];
+    if (m) {
+      const int t0 = __ffsll(static_cast<long long>(m)) - 1;
+      const int t1 = 63 - __clzll(static_cast<long long>(m));
+      const unsigned long long upto = (t1 >= 63) ? ~0ull : ((2ull << t1) - 1ull);
+      a.tile_mask[doff + j] = upto & ~((1ull << t0) - 1ull);
+    }
+  }
   int64_t acc = 0;
   for (int j = lo; j < hi; ++j) acc += 32 * __popcll(a.tile_mask[doff + j]);
   part[threadIdx.x] = acc;
