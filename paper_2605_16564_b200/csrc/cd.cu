@@ -232,15 +232,35 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
         cur_mk = mk;
         if (!KEEPW) return;
         if (TILES) {
-          // tile masks are contiguous ranges [k0, k0 + len) (tiles.cu): tile k
-          // sits at slot k - k0 of the staged column, tiles outside are zero
-          const int k0 = mk ? (__ffsll(static_cast<long long>(mk)) - 1) : 0;
-          const unsigned len = static_cast<unsigned>(__popcll(mk));
-          const double* base = col - 32 * k0 + lane;
+          // Tiles in groups of four with warp-uniform fast paths: RCB ordering
+          // makes kept tiles cluster, so most groups are all-kept (contiguous
+          // loads, no selects) or all-dropped (zeros).  Any mask shape.
+          int slot = 0;
 #pragma unroll
-          for (int k = 0; k < R; ++k) {
-            const bool in = static_cast<unsigned>(k - k0) < len;
-            w[k] = in ? base[32 * k] : 0.0;
+          for (int g = 0; g < (R + 3) / 4; ++g) {
+            const int cnt = (4 * g + 4 <= R) ? 4 : (R - 4 * g);
+            const unsigned full = (1u << cnt) - 1u;
+            const unsigned nib = static_cast<unsigned>(mk >> (4 * g)) & full;
+            if (nib == full) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (u < cnt) w[4 * g + u] = col[32 * (slot + u) + lane];
+              slot += cnt;
+            } else if (nib == 0u) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (u < cnt) w[4 * g + u] = 0.0;
+            } else {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                if (u < cnt) {
+                  const int bit = static_cast<int>((nib >> u) & 1u);
+                  const double v = col[32 * slot + lane];  // slot <= k < R: inside the ring slot
+                  w[4 * g + u] = bit ? v : 0.0;
+                  slot += bit;
+                }
+              }
+            }
           }
         } else {
 #pragma unroll
@@ -474,6 +494,415 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
   }
 }
 
+// ----------------------------------------------------------------------------
+// Lean tile-stream CD (default for tile-packed batches of <= 1024 rows).
+//
+// Same semantics and the same one-warp-per-fit / staged-ring design as
+// cd_kernel<..., TILES=true>, with the per-column instruction count cut down
+// (the generic tile kernel is issue-bound; profiles/r01_*):
+//  * columns are at most two contiguous runs of kept tiles (tiles.cu run
+//    cover), staged packed at the slot start; a lane addresses its tile with
+//    one of two bases instead of per-tile slot counting;
+//  * paired-row layout (R even): lane l owns packed rows 64q + 2l + {0,1}, so
+//    one 16-byte shared load feeds two registers (tile 2q + (l >> 4));
+//  * per-32-column chunk parameters (beta, col_sq, 1/(col_sq+lam2), run
+//    code, packed offset) are prefetched into registers one chunk ahead and
+//    published to a per-warp smem block: no global load on the column loop;
+//  * the issue path is one LDS + expect_tx + one bulk copy by lane 0 (TMA), or
+//    (CPA) per-lane 16-byte cp.async copies of exactly the words the lane
+//    reads later, which needs no mbarrier and no cross-lane hand-off.
+// Measured alternatives: placing tiles at their dense position
+// and clearing stale tiles (by zero-page bulk copies or by shared stores) so
+// loads need no predicates was 12-14% slower than predicated packed loads.
+
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void mbar_expect_s(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_s(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+// Run code of a tile mask made of at most two runs (tiles.cu run_cover):
+// a0 | la << 8 | b0 << 16 | lb << 24  (run A = tiles [a0, a0+la), B after it)
+__device__ __forceinline__ int tile_code(unsigned long long mk) {
+  if (mk == 0ull) return 0;
+  const int a0 = __ffsll(static_cast<long long>(mk)) - 1;
+  const unsigned long long x = ~(mk >> a0);
+  const int la = x ? (__ffsll(static_cast<long long>(x)) - 1) : 64 - a0;
+  const unsigned long long rest = (la >= 64) ? 0ull : (mk & ~(((1ull << la) - 1ull) << a0));
+  const int b0 = rest ? (__ffsll(static_cast<long long>(rest)) - 1) : 0;
+  return a0 | (la << 8) | (b0 << 16) | (__popcll(rest) << 24);
+}
+__device__ __forceinline__ int code_tiles(int code) {
+  return ((code >> 8) & 0xff) + ((code >> 24) & 0xff);
+}
+
+template <int R, int STAGES, int WPC, bool CPA>
+__global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
+  constexpr int SLOT = R * 32;  // doubles per ring slot (one dense column)
+  constexpr int PBLK = 144;     // doubles per warp: pb/pc/pinv[32] + pk/ioff/icode[32]
+  static_assert(R <= 32 && STAGES <= 8, "lean tile CD envelope");
+  constexpr bool VEC = (R % 2) == 0;
+  static_assert(!CPA || VEC, "per-lane async copies need the paired-row layout");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  double* const ring_all = reinterpret_cast<double*>(smem_raw);
+  double* const ring = ring_all + static_cast<size_t>(warp) * STAGES * SLOT;
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(ring_all + static_cast<size_t>(WPC) * STAGES * SLOT) +
+                         warp * STAGES;
+  double* const pb = reinterpret_cast<double*>(reinterpret_cast<uint64_t*>(
+                         ring_all + static_cast<size_t>(WPC) * STAGES * SLOT) + WPC * STAGES) +
+                     warp * PBLK;
+  double* const pc = pb + 32;
+  double* const pinv = pb + 64;
+  int* const pk = reinterpret_cast<int*>(pb + 96);  // consumer chunk: run codes
+  int* const ioff = pk + 32;                        // issue chunk: packed offsets (doubles)
+  int* const icode = pk + 64;                       // issue chunk: run codes
+  const uint32_t ring_s = smem_u32(ring);
+  const uint32_t bar_s = smem_u32(bars);
+  // this lane's tile in pair q is 2q + half (VEC) or k (scalar layout)
+  const int half = lane >> 4;
+
+  if (lane == 0) {
+    for (int i = 0; i < STAGES; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  int st = 0;       // consumer ring slot
+  uint32_t ph = 0;  // its mbarrier phase parity (TMA staging)
+  int ist = 0;      // issue ring slot
+  unsigned item = warp * gridDim.x + blockIdx.x;
+  const unsigned total_warps = gridDim.x * WPC;
+
+  while (item < a.S) {
+    const int64_t s = a.order ? a.order[item] : static_cast<int64_t>(item);
+    if (a.active == nullptr || a.active[s] != 0) {
+      const int64_t r0 = a.row_off[s];
+      const int N = static_cast<int>(a.row_off[s + 1] - r0);
+      const int M = a.m_cur[s];
+      const int64_t doff = a.dict_off[s];
+      const double* Ws = a.W + a.w_off[s];
+      const int64_t* colo = a.col_off + doff;
+      const unsigned long long* tmk = a.tile_mask + doff;
+      double* betas = a.beta + doff;
+      double* colsq = a.col_sq + doff;
+      const double lam1 = a.lam1[s], lam2 = a.lam2[s], tol = a.tol[s];
+      const int max_iters = a.max_iters[s];
+
+      double r[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int p = VEC ? (64 * (k >> 1) + 2 * lane + (k & 1)) : (lane + 32 * k);
+        const int row = a.perm ? (p < N ? a.perm[r0 + p] : 0) : p;
+        r[k] = (p < N) ? a.y[r0 + row] : 0.0;
+      }
+
+      // ---- issue side: column stream = [prologue M] + max_iters * M
+      // 32-bit stream counters: the host rejects M * (1 + max_iters) >= 2^31
+      const int total = M * (1 + max_iters);
+      int issued = 0;
+      int next_col = 0;
+      int pf_off = 0, pf_code = 0;  // issue parameters of the next chunk (lane = column)
+      auto fetch_issue = [&](int cb) {
+        const int c = cb + lane;
+        pf_off = (c < M) ? static_cast<int>(colo[c]) : 0;
+        pf_code = (c < M) ? tile_code(tmk[c]) : 0;
+      };
+      fetch_issue(0);
+      auto issue_one = [&]() {
+        const int c = next_col & 31;
+        if (c == 0) {
+          __syncwarp();
+          ioff[lane] = pf_off;
+          icode[lane] = pf_code;
+          __syncwarp();
+          fetch_issue(next_col + 32 < M ? next_col + 32 : 0);
+        }
+        if (CPA) {
+          // per-lane 16-byte async copies of exactly the words this lane reads
+          // later: pair q covers tile 2q + half at packed slot (t - a0) or
+          // (la + t - b0)
+          const int code = icode[c];
+          const int a0 = code & 0xff, la = (code >> 8) & 0xff;
+          const int b0 = (code >> 16) & 0xff, lb = code >> 24;
+          const int offA = ioff[c] - 32 * a0 + 2 * lane, offB = ioff[c] + 32 * (la - b0) + 2 * lane;
+          double* slot = ring + ist * SLOT;
+#pragma unroll
+          for (int q = 0; q < R / 2; ++q) {
+            const int t = 2 * q + half;
+            const bool inA = static_cast<unsigned>(t - a0) < static_cast<unsigned>(la);
+            const bool inB = static_cast<unsigned>(t - b0) < static_cast<unsigned>(lb);
+            const int o = (inA ? offA : offB) + 64 * q;
+            if (inA || inB) cp_async16(slot + (o - ioff[c]), Ws + o);
+          }
+          cp_async_commit();
+        } else if (lane == 0) {
+          const int code = icode[c];
+          const uint32_t bytes = static_cast<uint32_t>(code_tiles(code)) * 256u;
+          const uint32_t bar = bar_s + ist * 8;
+          if (bytes) {
+            mbar_expect_s(bar, bytes);
+            bulk_g2s(ring_s + ist * (SLOT * 8), Ws + ioff[c], bytes, bar);
+          } else {
+            mbar_arrive_s(bar);
+          }
+        }
+        if (++ist == STAGES) ist = 0;
+        ++issued;
+        if (++next_col == M) next_col = 0;
+      };
+      if (CPA) {
+        st = ist = 0;  // the previous item drained every copy group
+        for (int q = 0; q < STAGES; ++q) {
+          if (issued < total) issue_one();
+          else cp_async_commit();  // empty group: one group per stream position
+        }
+      } else {
+        for (int q = 0; q < STAGES && issued < total; ++q) issue_one();
+      }
+
+      // ---- consumer side
+      int consumed = 0;
+      double w[R];
+      auto load_w = [&](int code) {
+        const double* col = ring + st * SLOT;
+        if (CPA) cp_async_wait<STAGES - 1>();  // this lane's copies of the oldest group
+        else mbar_wait_s(bar_s + st * 8, ph);
+        const int a0 = code & 0xff, la = (code >> 8) & 0xff;
+        const int b0 = (code >> 16) & 0xff, lb = code >> 24;
+        if (VEC) {
+          const double* bA = col - 32 * a0 + 2 * lane;
+          const double* bB = col + 32 * (la - b0) + 2 * lane;
+#pragma unroll
+          for (int q = 0; q < R / 2; ++q) {
+            const int t = 2 * q + half;
+            const bool inA = static_cast<unsigned>(t - a0) < static_cast<unsigned>(la);
+            const bool inB = static_cast<unsigned>(t - b0) < static_cast<unsigned>(lb);
+            const double2* src = reinterpret_cast<const double2*>((inA ? bA : bB) + 64 * q);
+            const double2 v = (inA || inB) ? *src : make_double2(0.0, 0.0);
+            w[2 * q] = v.x;
+            w[2 * q + 1] = v.y;
+          }
+        } else {
+          const double* bA = col - 32 * a0 + lane;
+          const double* bB = col + 32 * (la - b0) + lane;
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            const bool inA = static_cast<unsigned>(k - a0) < static_cast<unsigned>(la);
+            const bool inB = static_cast<unsigned>(k - b0) < static_cast<unsigned>(lb);
+            w[k] = (inA || inB) ? (inA ? bA : bB)[32 * k] : 0.0;
+          }
+        }
+      };
+      auto advance = [&]() {
+        if (++st == STAGES) {
+          st = 0;
+          ph ^= 1u;
+        }
+        ++consumed;
+        if (issued < total) issue_one();
+        else if (CPA) cp_async_commit();
+      };
+
+      // prologue: col_sq (elastic_net.py:85) and r = y - W beta0 (elastic_net.py:94)
+      for (int cb = 0; cb < M; cb += 32) {
+        const int nc = min(32, M - cb);
+        int cl = 0;
+        double bl0 = 0.0, csl = 0.0;
+        if (lane < nc) {
+          cl = tile_code(tmk[cb + lane]);
+          bl0 = betas[cb + lane];
+        }
+        for (int t = 0; t < nc; ++t) {
+          load_w(__shfl_sync(0xffffffffu, cl, t));
+          double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            if (k & 1) p1 = fma(w[k], w[k], p1);
+            else p0 = fma(w[k], w[k], p0);
+          }
+          const double p = warp_sum(p0 + p1);
+          if (lane == t) csl = p;
+          const double b0 = __shfl_sync(0xffffffffu, bl0, t);
+          if (b0 != 0.0) {
+#pragma unroll
+            for (int k = 0; k < R; ++k) r[k] = fma(-b0, w[k], r[k]);
+          }
+          advance();
+        }
+        if (lane < nc) colsq[cb + lane] = csl;  // re-read below by the same lane
+      }
+
+      // sweeps (elastic_net.py:137-161); chunk parameters prefetched one chunk ahead
+      const bool one_chunk = M <= 32;
+      double nb_l = 0.0, ncs_l = 0.0;
+      int nk_l = 0;
+      auto fetch_params = [&](int cb) {
+        const int c = cb + lane;
+        nb_l = (c < M) ? betas[c] : 0.0;
+        ncs_l = (c < M) ? colsq[c] : 0.0;
+        nk_l = (c < M) ? tile_code(tmk[c]) : 0;
+      };
+      fetch_params(0);
+      int sweeps_done = 0, conv = 0;
+      double obj = 0.0;
+      for (int sw = 0; sw < max_iters; ++sw) {
+        double max_delta = 0.0, acc_l1 = 0.0, acc_l2 = 0.0, acc_max = 0.0;
+        for (int cb = 0; cb < M; cb += 32) {
+          const int nc = min(32, M - cb);
+          __syncwarp();
+          if (sw == 0 || !one_chunk) {
+            pb[lane] = nb_l;
+            pc[lane] = ncs_l;
+            const double dnv = __dadd_rn(ncs_l, lam2);
+            pinv[lane] = dnv > 0.0 ? __ddiv_rn(1.0, dnv) : 0.0;
+            pk[lane] = nk_l;
+            if (!one_chunk) fetch_params(cb + 32 < M ? cb + 32 : 0);
+          }
+          __syncwarp();
+          for (int t = 0; t < nc; ++t) {
+            load_w(pk[t]);
+            double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+              if (k & 1) d1 = fma(w[k], r[k], d1);
+              else d0 = fma(w[k], r[k], d0);
+            }
+            const double dot = warp_sum(d0 + d1);
+            const double b_old = pb[t];
+            const double cs = pc[t];
+            const double inv = pinv[t];
+            const double z = __dadd_rn(__dmul_rn(cs, b_old), dot);
+            double mag = __dsub_rn(fabs(z), lam1);
+            if (mag < 0.0) mag = 0.0;
+            const double num = z >= 0.0 ? mag : -mag;
+            // num / (cs + lam2) by the reciprocal and one FMA correction; a
+            // non-positive denominator has inv == 0 and yields b_new = 0
+            const double dn = __dadd_rn(cs, lam2);
+            const double q0 = __dmul_rn(num, inv);
+            const double b_new = fma(fma(-q0, dn, num), inv, q0);
+            const double d = __dsub_rn(b_new, b_old);
+#pragma unroll
+            for (int k = 0; k < R; ++k) r[k] = fma(-d, w[k], r[k]);
+            if (lane == 0) pb[t] = b_new;
+            const double ad = fabs(d);
+            max_delta = ad > max_delta ? ad : max_delta;  // fmax without the NaN fix-up
+            advance();
+          }
+          __syncwarp();
+          if (lane < nc) {
+            const double bl = pb[lane];
+            betas[cb + lane] = bl;
+            const double ab = fabs(bl);
+            acc_l1 += ab;
+            acc_l2 = fma(bl, bl, acc_l2);
+            acc_max = fmax(acc_max, ab);
+          }
+        }
+        double rss0 = 0.0, rss1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          if (k & 1) rss1 = fma(r[k], r[k], rss1);
+          else rss0 = fma(r[k], r[k], rss0);
+        }
+        const double rss = warp_sum(rss0 + rss1);
+        const double l1 = warp_sum(acc_l1);
+        const double l2 = warp_sum(acc_l2);
+        const double mabs = warp_max(acc_max);
+        obj = __dadd_rn(__dadd_rn(__dmul_rn(0.5, rss), __dmul_rn(lam1, l1)),
+                        __dmul_rn(__dmul_rn(0.5, lam2), l2));
+        if (a.hist != nullptr && lane == 0) a.hist[a.hist_off[s] + sw] = obj;
+        sweeps_done = sw + 1;
+        if (max_delta <= __dmul_rn(tol, fmax(mabs, 1.0))) {
+          conv = 1;
+          break;
+        }
+      }
+      if (max_iters == 0) {
+        // objective at the given beta (after the Gram-form sweeps, gram.cu)
+        double rss = 0.0, l1 = 0.0, l2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < R; ++k) rss = fma(r[k], r[k], rss);
+        rss = warp_sum(rss);
+        for (int j = lane; j < M; j += 32) {
+          const double b = betas[j];
+          l1 += fabs(b);
+          l2 = fma(b, b, l2);
+        }
+        l1 = warp_sum(l1);
+        l2 = warp_sum(l2);
+        obj = __dadd_rn(__dadd_rn(__dmul_rn(0.5, rss), __dmul_rn(lam1, l1)),
+                        __dmul_rn(__dmul_rn(0.5, lam2), l2));
+      }
+      // drain the prefetched columns of the sweep that will not run
+      if (CPA) {
+        cp_async_wait<0>();
+        consumed = issued;
+      }
+      while (consumed < issued) {
+        mbar_wait_s(bar_s + st * 8, ph);
+        if (++st == STAGES) {
+          st = 0;
+          ph ^= 1u;
+        }
+        ++consumed;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        a.sweeps[s] = sweeps_done;
+        a.converged[s] = conv;
+        a.objective[s] = obj;
+      }
+    }
+    unsigned nxt = 0;
+    if (lane == 0) nxt = atomicAdd(&g_cd_queue, 1u) + total_warps;
+    item = __shfl_sync(0xffffffffu, nxt, 0);
+  }
+}
+
+template <int R, int STAGES, int WPC, bool CPA = false>
+int launch_cd_tile(const CdArgs& a, cudaStream_t stream) {
+  const size_t smem = static_cast<size_t>(WPC) * STAGES * R * 32 * sizeof(double) +
+                      static_cast<size_t>(WPC) * STAGES * sizeof(uint64_t) +
+                      static_cast<size_t>(WPC) * 144 * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    PAM_CUDA_CHECK(cudaFuncSetAttribute(cd_tile_kernel<R, STAGES, WPC, CPA>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  int dev = 0, sms = 148;
+  PAM_CUDA_CHECK(cudaGetDevice(&dev));
+  PAM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  void* qaddr = nullptr;
+  PAM_CUDA_CHECK(cudaGetSymbolAddress(&qaddr, g_cd_queue));
+  PAM_CUDA_CHECK(cudaMemsetAsync(qaddr, 0, sizeof(unsigned), stream));
+  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(sms, a.S));
+  cd_tile_kernel<R, STAGES, WPC, CPA><<<(unsigned)ctas, WPC * 32, smem, stream>>>(a);
+  PAM_LAUNCH_CHECK("cd_tile_kernel");
+  return PAM_OK;
+}
+
 template <int R, int STAGES, int WPC, int G, bool TILES = false, bool KEEPW = true, bool LDGSTS = false>
 int launch_cd(const CdArgs& a, cudaStream_t stream) {
   constexpr int NGROUPS = WPC / G;
@@ -526,7 +955,26 @@ int cd_dispatch(const CdArgs& a, int max_rows, cudaStream_t stream) {
 }
 
 int cd_dispatch_tiles(const CdArgs& a, int max_rows, cudaStream_t stream) {
-  // one warp per subdomain; tile k of a column <-> register r[k] of every lane
+  // one warp per subdomain; tile k of a column <-> register r[k] of every lane.
+  // PAM_CD_LEAN: 1 (default) lean kernel with TMA staging; 3 lean kernel with
+  // per-lane cp.async staging; 0 the generic cd_kernel (any mask shape).  The
+  // lean kernels need masks of <= 2 runs (PAM_TILE_RUNS != 0).
+  const char* lean_env = getenv("PAM_CD_LEAN");
+  const int lean = (tile_runs() == 0) ? 0 : (lean_env ? atoi(lean_env) : 1);
+  if (lean == 3 && max_rows > 32 && max_rows <= 512) {
+    if (max_rows <= 64) return launch_cd_tile<2, 4, 16, true>(a, stream);
+    if (max_rows <= 128) return launch_cd_tile<4, 4, 16, true>(a, stream);
+    if (max_rows <= 256) return launch_cd_tile<8, 4, 16, true>(a, stream);
+    return launch_cd_tile<16, 3, 16, true>(a, stream);
+  }
+  if (lean == 1 || lean == 3) {
+    if (max_rows <= 32) return launch_cd_tile<1, 4, 16>(a, stream);
+    if (max_rows <= 64) return launch_cd_tile<2, 4, 16>(a, stream);
+    if (max_rows <= 128) return launch_cd_tile<4, 4, 16>(a, stream);
+    if (max_rows <= 256) return launch_cd_tile<8, 4, 16>(a, stream);
+    if (max_rows <= 512) return launch_cd_tile<16, 3, 16>(a, stream);
+    if (max_rows <= 1024) return launch_cd_tile<32, 3, 8>(a, stream);
+  }
   if (max_rows <= 32) return launch_cd<1, 4, 16, 1, true>(a, stream);
   if (max_rows <= 64) return launch_cd<2, 4, 16, 1, true>(a, stream);
   if (max_rows <= 128) return launch_cd<4, 4, 16, 1, true>(a, stream);

@@ -255,6 +255,10 @@ class FitEngine:
         self.dict_off = np.concatenate([[0], np.cumsum(self.cap)[:-1]]).astype(np.int64)
         cap_tot = int(self.cap.sum())
         self.form = cd_form(self.n_rows, self.cap)
+        # the device column stream (prologue + sweeps) is counted in 32 bits
+        if np.any(self.cap * (1 + p["max_iters"]) >= 2**31):
+            raise NotImplementedError("dictionary capacity x (max_iters + 1) >= 2^31 is outside the "
+                                      "CD kernel envelope")
         self.tau = tile_tau() if tau is None else float(tau)
         self.tiles = self.form == "residual" and self.tau > 0.0 and self.max_rows <= 1024
         self.ld = _round16(self.n_rows) if not self.tiles else (self.n_rows + 31) // 32 * 32

@@ -234,9 +234,12 @@ def test_tile_packed_stream_matches_dense(cuda, monkeypatch, cells):
             assert abs(x.rel_l2 - y.rel_l2) <= 1e-10 * x.rel_l2
 
 
-@pytest.mark.parametrize("variant", [{"PAM_CD_RING": "1"}, {"PAM_CD_COPY": "ldgsts"}])
+@pytest.mark.parametrize("variant", [{"PAM_CD_RING": "1"}, {"PAM_CD_LEAN": "0", "PAM_CD_COPY": "ldgsts"},
+                                     {"PAM_CD_LEAN": "0"}, {"PAM_CD_LEAN": "3"}, {"PAM_TILE_RUNS": "2"},
+                                     {"PAM_TILE_RUNS": "0"}])
 def test_cd_staging_variants_match(cuda, monkeypatch, variant):
-    """Opt-in CD staging variants (byte ring, LDGSTS) reproduce the default kernel."""
+    """Opt-in CD variants (byte ring, LDGSTS staging, generic tile kernel, per-lane
+    cp.async staging, two-run / exact tile masks) reproduce the default lean kernel."""
     field = pam.box_field_2d(40, 40)
     part = pam.make_partition(field.mesh, 2, 2)  # 400 rows: the R=16 tile kernels
     cfg = pam.AdaptiveConfig(k_top=40, m_max=240, m_q=3, max_rounds=3, elastic=EN_2D,
@@ -339,3 +342,18 @@ def test_subdomain_batch_api_c5_sample(cuda):
         o = O.fit_log(p.values[a:b], W, c.elastic.lam1, c.elastic.lam2, c.elastic.tol, c.elastic.max_iters)
         assert np.max(np.abs(res.beta[s] - o["beta"])) <= BETA_TOL * max(1, np.abs(o["beta"]).max())
         assert res.rounds[0].sweeps[s] == o["iterations"] or abs(res.rounds[0].sweeps[s] - o["iterations"]) <= 1
+
+
+def test_sharded_fit_single_rank_device_path(cuda):
+    """parallel.fit_parallel_sharded with the device fit_range (world size 1) == fit_parallel."""
+    from paper_2605_16564_b200 import parallel
+
+    field = pam.box_field_2d(16, 16)
+    part = pam.make_partition(field.mesh, 2, 2)
+    cfg = pam.AdaptiveConfig(k_top=12, m_max=72, m_q=3, max_rounds=3, elastic=EN_2D,
+                             offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
+    spec = pam.DictionarySpec(sigma=0.0625)
+    ref, rep = pam.fit_parallel(field, part, cfg, spec)
+    sh, reps = parallel.fit_parallel_sharded(field, part, cfg, spec)
+    assert pam.dumps(sh) == pam.dumps(ref)
+    assert [[r.centers for r in rr] for rr in reps] == [[r.centers for r in rr] for rr in rep.rounds]
