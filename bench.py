@@ -368,7 +368,7 @@ def run_ours(args):
         },
         "evals": {"value": world * P * args.steps / eval_s, "unit": "points/s",
                   "ms_per_step": eval_s / args.steps * 1e3},
-        "roofline": {"kernel": "cd_kernel (batched CD, TMA-streamed W)", "bound": "hbm",
+        "roofline": {"kernel": cd_kernel_name(), "bound": "hbm",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "peak_source": src, "traffic": None,
                      "algorithmic_bytes_per_launch": cd_bytes / max(cd_launches, 1),
@@ -386,6 +386,9 @@ def run_ours(args):
                           "peak": fp64_peak / 1e9, "peak_source": "measured (pam_probe_fp64, FMA=2)",
                           "frac": eval_pairs * 33 / (eval_s / args.steps) / fp64_peak},
         "kernel_seconds_per_step": {k: v / args.steps for k, v in kt.items()},
+        "cd_rounds": [{**d, "achieved_gbs": d["bytes"] / d["seconds"] / 1e9 if d["seconds"] else None,
+                       "max_over_mean_fit": d["max_fit_bytes"] / d["mean_fit_bytes"] if d["mean_fit_bytes"] else None}
+                      for d in recs[-1][0].device.get("cd_rounds", [])],
         "gpu_launches": launches,
         "clocks": clocks,
         "e2e": e2e,
@@ -393,11 +396,40 @@ def run_ours(args):
     }
     if args.traffic:
         line["roofline"]["traffic"] = float(args.traffic)
+    else:
+        tr = committed_traffic(line["roofline"]["kernel"])
+        if tr is not None:
+            line["roofline"]["traffic"] = tr["dram_bytes_per_launch"]
+            line["roofline"]["traffic_source"] = tr["source"]
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def cd_kernel_name() -> str:
+    """The CD kernel the tile path dispatches to under the current environment (cd.cu)."""
+    if os.environ.get("PAM_TILE_TAU") == "0":
+        return "cd_kernel (dense column stream, TMA)"
+    runs = os.environ.get("PAM_TILE_RUNS", "1")
+    lean = os.environ.get("PAM_CD_LEAN", "1")
+    if runs == "0" or lean == "0":
+        return "cd_kernel (generic tile stream, TMA)"
+    if os.environ.get("PAM_CD_PAIR", "0") == "1":
+        return "cd_pair_kernel (column-pair tile stream, TMA)"
+    return "cd_tile_kernel (single-column tile stream, TMA)"
+
+
+def committed_traffic(kernel: str):
+    """DRAM bytes per CD launch measured by ncu for this kernel (profiles/cd_traffic.json)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "cd_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+    except (OSError, ValueError):
+        return None
+    return d if d.get("kernel") == kernel else None
 
 
 def run_c5(args):

@@ -53,6 +53,7 @@ class RoundRecord:
     seconds: float
     ran: np.ndarray  # (S,) bool: subdomain produced a report this round
     stream_doubles: np.ndarray = None  # (S,) design-matrix doubles the CD streams per sweep
+    cd_seconds: float = 0.0  # device time of this round's CD launch (CUDA events)
 
 
 @dataclass
@@ -332,6 +333,7 @@ class FitEngine:
             self.d_rowsum = t.empty(ntot, dtype=f64, device=dev)
             self.d_tile_mask = t.zeros(cap_tot, dtype=i64, device=dev)
             self.d_col_off = t.zeros(cap_tot, dtype=i64, device=dev)
+            self.d_pair_dot = t.zeros(cap_tot, dtype=f64, device=dev)  # column-pair CD scratch
             self.d_packed = t.zeros(S, dtype=i64, device=dev)
 
         # ---- initial dictionary into the capacity slots
@@ -431,8 +433,8 @@ class FitEngine:
                     P(self.d_dict_off), P(self.d_m_cur), P(self.d_w_off), P(self.d_tile_mask),
                     P(self.d_col_off), P(self.d_W), P(self.d_lam1), P(self.d_lam2), P(self.d_tol),
                     P(self.d_max_iters), P(self.d_active), self.max_rows, P(self.d_beta),
-                    P(self.d_col_sq), P(self.d_sweeps), P(self.d_conv), P(self.d_obj), None, None, st),
-                    "pam_cd_tiles_f64")
+                    P(self.d_col_sq), P(self.d_sweeps), P(self.d_conv), P(self.d_obj), None, None,
+                    P(self.d_pair_dot), st), "pam_cd_tiles_f64")
             else:
                 nat.check(lib.pam_cd_f64(
                     len(order), P(d_order), P(self.d_row_off), P(self.d_y), P(self.d_dict_off),
@@ -471,6 +473,7 @@ class FitEngine:
                 rel_l2=rel, abs_l2=np.sqrt(num), objective=obj, sweeps=sweeps,
                 converged=conv.astype(bool), seconds=0.0, ran=active.copy(),
                 stream_doubles=np.asarray(stream_doubles, dtype=np.int64).copy(),
+                cd_seconds=e1.elapsed_time(e2) / 1e3,
             )
             # stop rules in the reference's order (adaptive.py:252-260)
             stop = (rmax < p["eps_tol"]) | (added_total >= p["m_max"]) | (rnd == p["max_rounds"] - 1)
@@ -597,7 +600,8 @@ def _merge_results(parts, offsets):
             abs_l2=cat("abs_l2", np.nan), objective=cat("objective", np.nan), sweeps=cat("sweeps", 0),
             converged=cat("converged", False), stream_doubles=cat("stream_doubles", 0),
             seconds=float(sum(p.rounds[k].seconds for p in parts if k < len(p.rounds))),
-            ran=cat("ran", False)))
+            ran=cat("ran", False),
+            cd_seconds=float(sum(p.rounds[k].cd_seconds for p in parts if k < len(p.rounds)))))
     kt = {}
     for p in parts:
         for key, v in p.kernel_seconds.items():

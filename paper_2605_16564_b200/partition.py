@@ -549,6 +549,12 @@ def _fit_range(data, partition, cfgs, specs, lo, hi):
             dstats["cd_flops"] += int(np.sum(4 * nm * sw))  # dot + axpy, 2 FMA per entry
             dstats["sweeps"] += int(sw.sum())
             dstats["cd_launches"] += 1
+            fit_bytes = 8 * nm * (sw + 1)
+            dstats.setdefault("cd_rounds", []).append({
+                "round": int(rec.round), "seconds": float(rec.cd_seconds), "fits": int(ran.sum()),
+                "bytes": int(fit_bytes.sum()),
+                "mean_fit_bytes": float(fit_bytes.mean()) if fit_bytes.size else 0.0,
+                "max_fit_bytes": int(fit_bytes.max()) if fit_bytes.size else 0})
         for s in range(b - a):
             i = a + s - lo
             d = RbfDictionary(centers=res.centres[s], widths=res.widths[s],

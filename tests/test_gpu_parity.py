@@ -235,11 +235,13 @@ def test_tile_packed_stream_matches_dense(cuda, monkeypatch, cells):
 
 
 @pytest.mark.parametrize("variant", [{"PAM_CD_RING": "1"}, {"PAM_CD_LEAN": "0", "PAM_CD_COPY": "ldgsts"},
-                                     {"PAM_CD_LEAN": "0"}, {"PAM_CD_LEAN": "3"}, {"PAM_TILE_RUNS": "2"},
+                                     {"PAM_CD_LEAN": "0"}, {"PAM_CD_PAIR": "1"},
+                                     {"PAM_CD_LEAN": "3"}, {"PAM_TILE_RUNS": "2"},
                                      {"PAM_TILE_RUNS": "0"}])
 def test_cd_staging_variants_match(cuda, monkeypatch, variant):
-    """Opt-in CD variants (byte ring, LDGSTS staging, generic tile kernel, per-lane
-    cp.async staging, two-run / exact tile masks) reproduce the default lean kernel."""
+    """Opt-in CD variants (byte ring, LDGSTS staging, generic tile kernel, column-pair
+    kernel, per-lane cp.async staging, two-run / exact tile masks) reproduce the default
+    single-column lean kernel."""
     field = pam.box_field_2d(40, 40)
     part = pam.make_partition(field.mesh, 2, 2)  # 400 rows: the R=16 tile kernels
     cfg = pam.AdaptiveConfig(k_top=40, m_max=240, m_q=3, max_rounds=3, elastic=EN_2D,
@@ -357,3 +359,24 @@ def test_sharded_fit_single_rank_device_path(cuda):
     sh, reps = parallel.fit_parallel_sharded(field, part, cfg, spec)
     assert pam.dumps(sh) == pam.dumps(ref)
     assert [[r.centers for r in rr] for rr in reps] == [[r.centers for r in rr] for rr in rep.rounds]
+
+
+@pytest.mark.parametrize("cells", [(20, 20), (30, 30)])
+def test_pair_kernel_odd_column_counts(cuda, monkeypatch, cells):
+    """Column-pair CD (opt-in) with odd dictionary sizes (unpaired tail column) == single-column CD."""
+    field = pam.box_field_2d(*cells)
+    part = pam.make_partition(field.mesh, 2, 2)  # 100 / 225 rows: the R=4 / R=8 pair kernels
+    cfg = pam.AdaptiveConfig(k_top=7, m_max=60, m_q=3, max_rounds=3, elastic=EN_2D,
+                             offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
+    spec = pam.DictionarySpec(sigma=0.5 / cells[0])
+    single, rs = pam.fit_parallel(field, part, cfg, spec)
+    monkeypatch.setenv("PAM_CD_PAIR", "1")
+    pair, rp = pam.fit_parallel(field, part, cfg, spec)
+    assert any(r.centers % 2 for reps in rp.rounds for r in reps)  # odd M was exercised
+    for a, b in zip(single.locals, pair.locals):
+        np.testing.assert_array_equal(a.dictionary.centers, b.dictionary.centers)
+        assert np.max(np.abs(a.beta - b.beta)) <= 1e-10 * max(1, np.abs(a.beta).max())
+    for ra, rb in zip(rs.rounds, rp.rounds):
+        for x, y in zip(ra, rb):
+            assert (x.centers, x.added) == (y.centers, y.added)
+            assert abs(x.objective - y.objective) <= 1e-10 * abs(x.objective)
