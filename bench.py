@@ -416,9 +416,7 @@ def cd_kernel_name() -> str:
     lean = os.environ.get("PAM_CD_LEAN", "1")
     if runs == "0" or lean == "0":
         return "cd_kernel (generic tile stream, TMA)"
-    if os.environ.get("PAM_CD_PAIR", "0") == "1":
-        return "cd_pair_kernel (column-pair tile stream, TMA)"
-    return "cd_tile_kernel (single-column tile stream, TMA)"
+    return "cd_tile_kernel (lean single-column tile stream, TMA)"
 
 
 def committed_traffic(kernel: str):

@@ -145,8 +145,7 @@ int pam_cd_ex_f64(int64_t S, const int64_t* order, const int64_t* row_off, doubl
  * PAM_TILE_RUNS (default 1) contiguous runs of tiles (holes stored as their
  * exact small values).  pam_cd_tiles_f64 is pam_cd_f64 over that layout: one
  * cp.async.bulk of popcount(mask)*256 bytes per column; y is read through
- * perm.  pair_dot (nullable, one double per slot) is scratch for the
- * column-pair kernel (W_j . W_{j+1}); NULL selects the single-column kernel. */
+ * perm. */
 int pam_assemble_tiles_f64(int dim, int64_t S, const int64_t* row_off, const double* pts,
                            const int32_t* perm, const int64_t* dict_off, const int32_t* m_cur,
                            const double* centres, const double* widths, const int64_t* w_off,
@@ -159,8 +158,7 @@ int pam_cd_tiles_f64(int64_t S, const int64_t* order, const int64_t* row_off, co
                      const double* W, const double* lam1, const double* lam2, const double* tol,
                      const int32_t* max_iters, const int32_t* active, int32_t max_rows,
                      double* beta, double* col_sq, int32_t* sweeps, int32_t* converged,
-                     double* objective, double* hist, const int64_t* hist_off, double* pair_dot,
-                     void* stream);
+                     double* objective, double* hist, const int64_t* hist_off, void* stream);
 
 /* ---- K2 + K2b': Gram products and the Gram-form CD (M < N) -----------------
  * pam_gram_f64: G_s = W_s^T W_s (symmetric, column-major at G + g_off[s],

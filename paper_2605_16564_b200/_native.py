@@ -66,7 +66,7 @@ SIGNATURES = {
     "pam_cd_tiles_f64": (
         ctypes.c_int,
         [_i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr,
-         _ptr, _i32, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr],
+         _ptr, _i32, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr],
     ),
     "pam_gram_f64": (
         ctypes.c_int,

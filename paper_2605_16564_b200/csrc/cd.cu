@@ -61,7 +61,6 @@ struct CdArgs {
   const unsigned long long* tile_mask;
   const int64_t* col_off;
   const int32_t* perm;  // tile mode: packed position -> local row (nullable = identity)
-  double* pair_dot;     // tile mode: per-slot scratch for W_j . W_{j+1} (nullable)
 };
 
 // named barrier over the G warps of one subdomain group (G > 1 only)
@@ -528,6 +527,17 @@ __device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t parity) {
         : "memory");
   } while (!ok);
 }
+__device__ __forceinline__ bool mbar_test_s(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_expect_s(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
@@ -715,11 +725,12 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
 
       // ---- consumer side
       int consumed = 0;
+      bool ready = false;  // next slot's mbarrier phase already observed complete
       double w[R];
       auto load_w = [&](int code) {
         const double* col = ring + st * SLOT;
         if (CPA) cp_async_wait<STAGES - 1>();  // this lane's copies of the oldest group
-        else mbar_wait_s(bar_s + st * 8, ph);
+        else if (!ready) mbar_wait_s(bar_s + st * 8, ph);
         const int a0 = code & 0xff, la = (code >> 8) & 0xff;
         const int b0 = (code >> 16) & 0xff, lb = code >> 24;
         if (VEC && !CPA) {
@@ -774,6 +785,9 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
           ph ^= 1u;
         }
         ++consumed;
+        // non-blocking look at the next slot now, so the barrier round trip
+        // overlaps the reduction and update of this column
+        if (!CPA) ready = (consumed < issued) && mbar_test_s(bar_s + st * 8, ph);
       };
 
       // prologue: col_sq (elastic_net.py:85) and r = y - W beta0 (elastic_net.py:94)
@@ -835,27 +849,34 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
           __syncwarp();
           for (int t = 0; t < nc; ++t) {
             load_w(pk[t]);
-            double d0 = 0.0, d1 = 0.0;
+            // four independent FMA chains: the dot sits on the per-column critical path
+            double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
 #pragma unroll
             for (int k = 0; k < R; ++k) {
-              if (k & 1) d1 = fma(w[k], r[k], d1);
-              else d0 = fma(w[k], r[k], d0);
+              if ((k & 3) == 0) d0 = fma(w[k], r[k], d0);
+              else if ((k & 3) == 1) d1 = fma(w[k], r[k], d1);
+              else if ((k & 3) == 2) d2 = fma(w[k], r[k], d2);
+              else d3 = fma(w[k], r[k], d3);
             }
-            const double part = d0 + d1;
+            const double part = (d0 + d1) + (d2 + d3);
             advance(part);  // slot free once its words are in registers
-            const double dot = warp_sum(part);
             const double b_old = pb[t];
             const double cs = pc[t];
             const double inv = pinv[t];
-            const double z = __dadd_rn(__dmul_rn(cs, b_old), dot);
-            double mag = __dsub_rn(fabs(z), lam1);
-            if (mag < 0.0) mag = 0.0;
-            const double num = z >= 0.0 ? mag : -mag;
-            // num / (cs + lam2) by the reciprocal and one FMA correction; a
-            // non-positive denominator has inv == 0 and yields b_new = 0
+            const double cb_old = __dmul_rn(cs, b_old);  // off the dot's critical path
             const double dn = __dadd_rn(cs, lam2);
-            const double q0 = __dmul_rn(num, inv);
-            const double b_new = fma(fma(-q0, dn, num), inv, q0);
+            const double dot = warp_sum(part);
+            const double z = __dadd_rn(cb_old, dot);
+            // soft threshold sign(z) max(|z| - lam1, 0) with both signed numerators
+            // formed in parallel (z - lam1 == |z| - lam1 for z > 0, z + lam1 ==
+            // -(|z| - lam1) for z < 0, exactly), then num / (cs + lam2) by the
+            // reciprocal and one FMA correction; inv == 0 (non-positive
+            // denominator) yields 0
+            const double np_ = __dsub_rn(z, lam1), nn_ = __dadd_rn(z, lam1);
+            const double qp = __dmul_rn(np_, inv), qn = __dmul_rn(nn_, inv);
+            const double bp = fma(fma(-qp, dn, np_), inv, qp);
+            const double bn = fma(fma(-qn, dn, nn_), inv, qn);
+            const double b_new = np_ > 0.0 ? bp : (nn_ < 0.0 ? bn : 0.0);
             const double d = __dsub_rn(b_new, b_old);
 #pragma unroll
             for (int k = 0; k < R; ++k) r[k] = fma(-d, w[k], r[k]);
@@ -966,379 +987,6 @@ int launch_cd_tile_r(const CdArgs& a, cudaStream_t stream) {
   return PAM_OK;
 }
 
-// ----------------------------------------------------------------------------
-// Column-pair tile CD (default for tile-packed batches of 65..512 rows when a
-// pair scratch is given).
-//
-// The cyclic order is kept: column j+1 sees the residual after column j's
-// update, but its dot product is formed as W_{j+1}.r - d_j (W_j . W_{j+1})
-// from the pre-update residual, with the pair product c_j = W_j . W_{j+1}
-// computed once per fit in the prologue pass (the columns are fixed during a
-// fit).  Both dot products of a pair then share one load phase, one
-// transposed 5-level shuffle reduction (instead of two) and one AXPY phase,
-// which roughly halves the per-column bookkeeping of the issue-bound
-// single-column kernel.  Rounding differs from the sequential form only in
-// the order of the length-N sums (the parity tolerance of SURVEY F2).
-// Tile masks of up to two runs (tiles.cu run_cover); tiles outside both runs
-// read a shared zero block instead of being predicated and zeroed.
-template <int R, int SLOTS, int WPC, int RUNS>
-__global__ void __launch_bounds__(WPC * 32, 1) cd_pair_kernel(const CdArgs a) {
-  constexpr int SLOT = R * 32;  // doubles per ring slot (one dense column)
-  constexpr int PBLK = 160;     // doubles per warp: pb/pc/pinv[32] + pcc[16] + pk/ioff/icode[32]
-  static_assert(R % 2 == 0 && R <= 32 && SLOTS >= 4 && SLOTS % 2 == 0, "pair CD envelope");
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  double* const ring_all = reinterpret_cast<double*>(smem_raw);
-  double* const ring = ring_all + static_cast<size_t>(warp) * SLOTS * SLOT;
-  uint64_t* const bars_all = reinterpret_cast<uint64_t*>(ring_all + static_cast<size_t>(WPC) * SLOTS * SLOT);
-  uint64_t* const bars = bars_all + warp * SLOTS;
-  double* const zero_blk = reinterpret_cast<double*>(bars_all + WPC * SLOTS);  // SLOT doubles of zeros
-  double* const pb = zero_blk + SLOT + warp * PBLK;
-  double* const pc = pb + 32;
-  double* const pinv = pb + 64;
-  double* const pcc = pb + 96;                       // pair products of the chunk's 16 pairs
-  int* const pk = reinterpret_cast<int*>(pb + 112);  // consumer chunk: run codes
-  int* const ioff = pk + 32;                         // issue chunk: packed offsets (doubles)
-  int* const icode = pk + 64;                        // issue chunk: run codes
-  const uint32_t ring_s = smem_u32(ring);
-  const uint32_t bar_s = smem_u32(bars);
-  const int half = lane >> 4;  // this lane's tile in pair-row group q is 2q + half
-
-  for (int i = threadIdx.x; i < SLOT; i += WPC * 32) zero_blk[i] = 0.0;
-  if (lane == 0) {
-    for (int i = 0; i < SLOTS; ++i) mbar_init(&bars[i], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  int st = 0;       // consumer ring slot
-  uint32_t ph = 0;  // its mbarrier phase parity
-  int ist = 0;      // issue ring slot
-  unsigned item = warp * gridDim.x + blockIdx.x;
-  const unsigned total_warps = gridDim.x * WPC;
-
-  while (item < a.S) {
-    const int64_t s = a.order ? a.order[item] : static_cast<int64_t>(item);
-    if (a.active == nullptr || a.active[s] != 0) {
-      const int64_t r0 = a.row_off[s];
-      const int N = static_cast<int>(a.row_off[s + 1] - r0);
-      const int M = a.m_cur[s];
-      const int64_t doff = a.dict_off[s];
-      const double* Ws = a.W + a.w_off[s];
-      const int64_t* colo = a.col_off + doff;
-      const unsigned long long* tmk = a.tile_mask + doff;
-      double* betas = a.beta + doff;
-      double* colsq = a.col_sq + doff;
-      double* pdot = a.pair_dot + doff;
-      const double lam1 = a.lam1[s], lam2 = a.lam2[s], tol = a.tol[s];
-      const int max_iters = a.max_iters[s];
-
-      // lane l holds packed rows 64q + 2l + {0,1} in registers 2q, 2q+1
-      double r[R];
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        const int p = 64 * (k >> 1) + 2 * lane + (k & 1);
-        const int row = a.perm ? (p < N ? a.perm[r0 + p] : 0) : p;
-        r[k] = (p < N) ? a.y[r0 + row] : 0.0;
-      }
-
-      // ---- issue side (one bulk copy per column, SLOTS columns ahead)
-      const int total = M * (1 + max_iters);  // host rejects >= 2^31
-      int issued = 0;
-      int next_col = 0;
-      int pf_off = 0, pf_code = 0;
-      auto fetch_issue = [&](int cb) {
-        const int c = cb + lane;
-        pf_off = (c < M) ? static_cast<int>(colo[c]) : 0;
-        pf_code = (c < M) ? tile_code(tmk[c]) : 0;
-      };
-      fetch_issue(0);
-      auto issue_one = [&]() {
-        const int c = next_col & 31;
-        if (c == 0) {
-          __syncwarp();
-          ioff[lane] = pf_off;
-          icode[lane] = pf_code;
-          __syncwarp();
-          fetch_issue(next_col + 32 < M ? next_col + 32 : 0);
-        }
-        if (lane == 0) {
-          const uint32_t bytes = static_cast<uint32_t>(code_tiles(icode[c])) * 256u;
-          const uint32_t bar = bar_s + ist * 8;
-          if (bytes) {
-            mbar_expect_s(bar, bytes);
-            bulk_g2s(ring_s + ist * (SLOT * 8), Ws + ioff[c], bytes, bar);
-          } else {
-            mbar_arrive_s(bar);
-          }
-        }
-        if (++ist == SLOTS) ist = 0;
-        ++issued;
-        if (++next_col == M) next_col = 0;
-      };
-      for (int q = 0; q < SLOTS && issued < total; ++q) issue_one();
-
-      // ---- consumer side
-      int consumed = 0;
-      // wait for the column in ring slot `slot` and load it (run code `code`):
-      // branch-free integer offsets from col + 2 lane; tiles outside both runs
-      // read the zero block (placed so that the same +64q offsets apply)
-      // (slot < 0: no column, all tiles read the zero block -- the odd tail)
-      auto load_col = [&](double (&w)[R], int slot, int code) {
-        const double* col = ring + max(slot, 0) * SLOT + 2 * lane;
-        if (slot >= 0) mbar_wait_s(bar_s + slot * 8, ph ^ (slot < st ? 1u : 0u));
-        const int a0 = code & 0xff, la = (code >> 8) & 0xff;
-        const int offA = -32 * a0;
-        const int offZ = static_cast<int>(zero_blk - (ring + max(slot, 0) * SLOT));
-        const int hA = half - a0;
-        const int b0 = (code >> 16) & 0xff, lb = code >> 24;
-        const int offB = 32 * (la - b0), hB = half - b0;
-#pragma unroll
-        for (int q = 0; q < R / 2; ++q) {
-          const bool inA = static_cast<unsigned>(hA + 2 * q) < static_cast<unsigned>(la);
-          int o;
-          if (RUNS == 1) {
-            o = inA ? offA : offZ;
-          } else {
-            const bool inB = static_cast<unsigned>(hB + 2 * q) < static_cast<unsigned>(lb);
-            o = (inA | inB) ? (inA ? offA : offB) : offZ;
-          }
-          const double2 v = *reinterpret_cast<const double2*>(col + o + 64 * q);
-          w[2 * q] = v.x;
-          w[2 * q + 1] = v.y;
-        }
-      };
-      auto advance = [&](int n) {
-        for (int i = 0; i < n; ++i) {
-          if (++st == SLOTS) {
-            st = 0;
-            ph ^= 1u;
-          }
-          ++consumed;
-        }
-        for (int i = 0; i < n; ++i)
-          if (issued < total) issue_one();
-      };
-      // transposed reduction: lanes 0-15 end with sum(x), lanes 16-31 with sum(y)
-      auto pair_sum = [&](double x, double y, double& sx, double& sy) {
-        double keep = half ? y : x;
-        const double send = half ? x : y;
-        keep += __shfl_xor_sync(0xffffffffu, send, 16);
-#pragma unroll
-        for (int o = 8; o > 0; o >>= 1) keep += __shfl_xor_sync(0xffffffffu, keep, o);
-        sx = __shfl_sync(0xffffffffu, keep, 0);
-        sy = __shfl_sync(0xffffffffu, keep, 16);
-      };
-
-      double wA[R], wB[R];
-      // prologue: col_sq (elastic_net.py:85), r = y - W beta0 (elastic_net.py:94)
-      // and the pair products c_j = W_j . W_{j+1} (j even)
-      for (int cb = 0; cb < M; cb += 32) {
-        const int nc = min(32, M - cb);
-        int cl = 0;
-        double bl0 = 0.0, csl = 0.0, ccl = 0.0;
-        if (lane < nc) {
-          cl = tile_code(tmk[cb + lane]);
-          bl0 = betas[cb + lane];
-        }
-        for (int t = 0; t < nc; t += 2) {
-          const bool two = t + 1 < nc;
-          load_col(wA, st, __shfl_sync(0xffffffffu, cl, t));
-          load_col(wB, two ? (st + 1 < SLOTS ? st + 1 : 0) : -1,
-                   two ? __shfl_sync(0xffffffffu, cl, t + 1) : 0);
-          double pa = 0.0, pbq = 0.0, pab = 0.0;
-#pragma unroll
-          for (int k = 0; k < R; ++k) {
-            pa = fma(wA[k], wA[k], pa);
-            pbq = fma(wB[k], wB[k], pbq);
-            pab = fma(wA[k], wB[k], pab);
-          }
-          pa = warp_sum(pa);
-          pbq = warp_sum(pbq);
-          pab = warp_sum(pab);
-          if (lane == t) {
-            csl = pa;
-            ccl = pab;
-          }
-          if (two && lane == t + 1) csl = pbq;
-          const double b0a = __shfl_sync(0xffffffffu, bl0, t);
-          const double b0b = two ? __shfl_sync(0xffffffffu, bl0, t + 1) : 0.0;
-          if (b0a != 0.0 || b0b != 0.0) {
-#pragma unroll
-            for (int k = 0; k < R; ++k) r[k] = fma(-b0b, wB[k], fma(-b0a, wA[k], r[k]));
-          }
-          advance(two ? 2 : 1);
-        }
-        if (lane < nc) {
-          colsq[cb + lane] = csl;  // re-read below by the same lane
-          pdot[cb + lane] = ccl;   // even lanes: c_j; odd lanes: unused
-        }
-      }
-
-      // sweeps (elastic_net.py:137-161) in column pairs
-      const bool one_chunk = M <= 32;
-      double nb_l = 0.0, ncs_l = 0.0, ncc_l = 0.0;
-      int nk_l = 0;
-      auto fetch_params = [&](int cb) {
-        const int c = cb + lane;
-        nb_l = (c < M) ? betas[c] : 0.0;
-        ncs_l = (c < M) ? colsq[c] : 0.0;
-        ncc_l = (c < M) ? pdot[c] : 0.0;
-        nk_l = (c < M) ? tile_code(tmk[c]) : 0;
-      };
-      fetch_params(0);
-      int sweeps_done = 0, conv = 0;
-      double obj = 0.0;
-      for (int sw = 0; sw < max_iters; ++sw) {
-        double max_delta = 0.0, acc_l1 = 0.0, acc_l2 = 0.0, acc_max = 0.0;
-        for (int cb = 0; cb < M; cb += 32) {
-          const int nc = min(32, M - cb);
-          __syncwarp();
-          if (sw == 0 || !one_chunk) {
-            pb[lane] = nb_l;
-            pc[lane] = ncs_l;
-            const double dnv = __dadd_rn(ncs_l, lam2);
-            pinv[lane] = dnv > 0.0 ? __ddiv_rn(1.0, dnv) : 0.0;
-            if (!(lane & 1)) pcc[lane >> 1] = ncc_l;
-            pk[lane] = nk_l;
-            if (!one_chunk) fetch_params(cb + 32 < M ? cb + 32 : 0);
-          }
-          __syncwarp();
-          for (int t = 0; t < nc; t += 2) {
-            const bool two = t + 1 < nc;  // warp-uniform; false only for the odd tail
-            load_col(wA, st, pk[t]);
-            load_col(wB, two ? (st + 1 < SLOTS ? st + 1 : 0) : -1, two ? pk[t + 1] : 0);
-            double ga0 = 0.0, ga1 = 0.0, gb0 = 0.0, gb1 = 0.0;
-#pragma unroll
-            for (int k = 0; k < R; ++k) {
-              if (k & 1) {
-                ga1 = fma(wA[k], r[k], ga1);
-                gb1 = fma(wB[k], r[k], gb1);
-              } else {
-                ga0 = fma(wA[k], r[k], ga0);
-                gb0 = fma(wB[k], r[k], gb0);
-              }
-            }
-            double gA, gB;
-            pair_sum(ga0 + ga1, gb0 + gb1, gA, gB);
-            const double2 bo = *reinterpret_cast<const double2*>(pb + t);
-            const double2 cs = *reinterpret_cast<const double2*>(pc + t);
-            const double2 iv = *reinterpret_cast<const double2*>(pinv + t);
-            // column j = cb + t
-            double zA = __dadd_rn(__dmul_rn(cs.x, bo.x), gA);
-            double mag = __dsub_rn(fabs(zA), lam1);
-            if (mag < 0.0) mag = 0.0;
-            double num = zA >= 0.0 ? mag : -mag;
-            double dn = __dadd_rn(cs.x, lam2);
-            double q0 = __dmul_rn(num, iv.x);
-            const double bA_new = fma(fma(-q0, dn, num), iv.x, q0);
-            const double dA = __dsub_rn(bA_new, bo.x);
-            // column j + 1 sees the residual after column j: W_{j+1}.(r - dA W_j)
-            const double gB1 = fma(-dA, pcc[t >> 1], gB);
-            const double zB = __dadd_rn(__dmul_rn(cs.y, bo.y), gB1);
-            mag = __dsub_rn(fabs(zB), lam1);
-            if (mag < 0.0) mag = 0.0;
-            num = zB >= 0.0 ? mag : -mag;
-            dn = __dadd_rn(cs.y, lam2);
-            q0 = __dmul_rn(num, iv.y);
-            const double bB_new = two ? fma(fma(-q0, dn, num), iv.y, q0) : bo.y;
-            const double dB = __dsub_rn(bB_new, bo.y);
-#pragma unroll
-            for (int k = 0; k < R; ++k) r[k] = fma(-dB, wB[k], fma(-dA, wA[k], r[k]));
-            if (lane == 0) *reinterpret_cast<double2*>(pb + t) = make_double2(bA_new, bB_new);
-            const double ad = fmax(fabs(dA), fabs(dB));
-            max_delta = ad > max_delta ? ad : max_delta;
-            advance(two ? 2 : 1);
-          }
-          __syncwarp();
-          if (lane < nc) {
-            const double bl = pb[lane];
-            betas[cb + lane] = bl;
-            const double ab = fabs(bl);
-            acc_l1 += ab;
-            acc_l2 = fma(bl, bl, acc_l2);
-            acc_max = fmax(acc_max, ab);
-          }
-        }
-        double rss0 = 0.0, rss1 = 0.0;
-#pragma unroll
-        for (int k = 0; k < R; ++k) {
-          if (k & 1) rss1 = fma(r[k], r[k], rss1);
-          else rss0 = fma(r[k], r[k], rss0);
-        }
-        const double rss = warp_sum(rss0 + rss1);
-        const double l1 = warp_sum(acc_l1);
-        const double l2 = warp_sum(acc_l2);
-        const double mabs = warp_max(acc_max);
-        obj = __dadd_rn(__dadd_rn(__dmul_rn(0.5, rss), __dmul_rn(lam1, l1)),
-                        __dmul_rn(__dmul_rn(0.5, lam2), l2));
-        if (a.hist != nullptr && lane == 0) a.hist[a.hist_off[s] + sw] = obj;
-        sweeps_done = sw + 1;
-        if (max_delta <= __dmul_rn(tol, fmax(mabs, 1.0))) {
-          conv = 1;
-          break;
-        }
-      }
-      if (max_iters == 0) {
-        double rss = 0.0, l1 = 0.0, l2 = 0.0;
-#pragma unroll
-        for (int k = 0; k < R; ++k) rss = fma(r[k], r[k], rss);
-        rss = warp_sum(rss);
-        for (int j = lane; j < M; j += 32) {
-          const double b = betas[j];
-          l1 += fabs(b);
-          l2 = fma(b, b, l2);
-        }
-        l1 = warp_sum(l1);
-        l2 = warp_sum(l2);
-        obj = __dadd_rn(__dadd_rn(__dmul_rn(0.5, rss), __dmul_rn(lam1, l1)),
-                        __dmul_rn(__dmul_rn(0.5, lam2), l2));
-      }
-      while (consumed < issued) {  // drain the prefetched columns of the unrun sweep
-        mbar_wait_s(bar_s + st * 8, ph);
-        if (++st == SLOTS) {
-          st = 0;
-          ph ^= 1u;
-        }
-        ++consumed;
-      }
-      __syncwarp();
-      if (lane == 0) {
-        a.sweeps[s] = sweeps_done;
-        a.converged[s] = conv;
-        a.objective[s] = obj;
-      }
-    }
-    unsigned nxt = 0;
-    if (lane == 0) nxt = atomicAdd(&g_cd_queue, 1u) + total_warps;
-    item = __shfl_sync(0xffffffffu, nxt, 0);
-  }
-}
-
-template <int R, int SLOTS, int WPC, int RUNS>
-int launch_cd_pair(const CdArgs& a, cudaStream_t stream) {
-  const size_t smem = static_cast<size_t>(WPC) * SLOTS * R * 32 * sizeof(double) +
-                      static_cast<size_t>(WPC) * SLOTS * sizeof(uint64_t) + R * 32 * sizeof(double) +
-                      static_cast<size_t>(WPC) * 160 * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    PAM_CUDA_CHECK(cudaFuncSetAttribute(cd_pair_kernel<R, SLOTS, WPC, RUNS>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
-  int dev = 0, sms = 148;
-  PAM_CUDA_CHECK(cudaGetDevice(&dev));
-  PAM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  void* qaddr = nullptr;
-  PAM_CUDA_CHECK(cudaGetSymbolAddress(&qaddr, g_cd_queue));
-  PAM_CUDA_CHECK(cudaMemsetAsync(qaddr, 0, sizeof(unsigned), stream));
-  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(sms, a.S));
-  cd_pair_kernel<R, SLOTS, WPC, RUNS><<<(unsigned)ctas, WPC * 32, smem, stream>>>(a);
-  PAM_LAUNCH_CHECK("cd_pair_kernel");
-  return PAM_OK;
-}
-
 template <int R, int STAGES, int WPC, int G, bool TILES = false, bool KEEPW = true, bool LDGSTS = false>
 int launch_cd(const CdArgs& a, cudaStream_t stream) {
   constexpr int NGROUPS = WPC / G;
@@ -1397,22 +1045,6 @@ int cd_dispatch_tiles(const CdArgs& a, int max_rows, cudaStream_t stream) {
   // lean kernels need masks of <= 2 runs (PAM_TILE_RUNS != 0).
   const char* lean_env = getenv("PAM_CD_LEAN");
   const int lean = (tile_runs() == 0) ? 0 : (lean_env ? atoi(lean_env) : 1);
-  const char* pair_env = getenv("PAM_CD_PAIR");
-  // column-pair kernel: opt-in (PAM_CD_PAIR=1); measured slower at C4
-  const bool pair = a.pair_dot != nullptr && lean != 0 && pair_env && atoi(pair_env) == 1;
-  if (pair && max_rows > 32 && max_rows <= 512) {
-    // four single-column ring slots per warp (a pair in use, a pair in flight)
-    if (tile_runs() == 2) {
-      if (max_rows <= 64) return launch_cd_pair<2, 4, 16, 2>(a, stream);
-      if (max_rows <= 128) return launch_cd_pair<4, 4, 16, 2>(a, stream);
-      if (max_rows <= 256) return launch_cd_pair<8, 4, 16, 2>(a, stream);
-      return launch_cd_pair<16, 4, 12, 2>(a, stream);
-    }
-    if (max_rows <= 64) return launch_cd_pair<2, 4, 16, 1>(a, stream);
-    if (max_rows <= 128) return launch_cd_pair<4, 4, 16, 1>(a, stream);
-    if (max_rows <= 256) return launch_cd_pair<8, 4, 16, 1>(a, stream);
-    return launch_cd_pair<16, 4, 12, 1>(a, stream);  // ~168 registers: 12 warps per SM
-  }
   if (lean == 3 && max_rows > 32 && max_rows <= 512) {
     if (max_rows <= 64) return launch_cd_tile<2, 4, 16, true>(a, stream);
     if (max_rows <= 128) return launch_cd_tile<4, 4, 16, true>(a, stream);
@@ -1424,7 +1056,11 @@ int cd_dispatch_tiles(const CdArgs& a, int max_rows, cudaStream_t stream) {
     if (max_rows <= 64) return launch_cd_tile<2, 4, 16>(a, stream);
     if (max_rows <= 128) return launch_cd_tile<4, 4, 16>(a, stream);
     if (max_rows <= 256) return launch_cd_tile<8, 4, 16>(a, stream);
-    if (max_rows <= 512) return launch_cd_tile<16, 3, 16>(a, stream);
+    if (max_rows <= 512) {
+      const char* se = getenv("PAM_CD_STAGES");
+      if (se && atoi(se) == 4) return launch_cd_tile<16, 4, 12>(a, stream);  // deeper ring, 12 warps
+      return launch_cd_tile<16, 3, 16>(a, stream);
+    }
     if (max_rows <= 1024) return launch_cd_tile<32, 3, 8>(a, stream);
   }
   if (max_rows <= 32) return launch_cd<1, 4, 16, 1, true>(a, stream);
@@ -1483,7 +1119,7 @@ extern "C" int pam_cd_tiles_f64(int64_t S, const int64_t* order, const int64_t* 
                                 const int32_t* max_iters, const int32_t* active, int32_t max_rows,
                                 double* beta, double* col_sq, int32_t* sweeps, int32_t* converged,
                                 double* objective, double* hist, const int64_t* hist_off,
-                                double* pair_dot, void* stream) {
+                                void* stream) {
   if (S < 0 || max_rows < 0 || !tile_mask || !col_off) return PAM_ERR_ARG;
   if (S == 0) return PAM_OK;
   const char* ring_env = getenv("PAM_CD_RING");
@@ -1494,7 +1130,7 @@ extern "C" int pam_cd_tiles_f64(int64_t S, const int64_t* order, const int64_t* 
   CdArgs a{S,      order,     row_off,   const_cast<double*>(y), dict_off, m_cur, w_off, m_cur,
            W,      lam1,      lam2,      tol,       max_iters, active, beta,   col_sq,
            sweeps, converged, objective, hist,      hist_off,  0,
-           reinterpret_cast<const unsigned long long*>(tile_mask), col_off, perm, pair_dot};
+           reinterpret_cast<const unsigned long long*>(tile_mask), col_off, perm};
   return cd_dispatch_tiles(a, max_rows, as_stream(stream));
 }
 

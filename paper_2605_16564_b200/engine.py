@@ -333,7 +333,6 @@ class FitEngine:
             self.d_rowsum = t.empty(ntot, dtype=f64, device=dev)
             self.d_tile_mask = t.zeros(cap_tot, dtype=i64, device=dev)
             self.d_col_off = t.zeros(cap_tot, dtype=i64, device=dev)
-            self.d_pair_dot = t.zeros(cap_tot, dtype=f64, device=dev)  # column-pair CD scratch
             self.d_packed = t.zeros(S, dtype=i64, device=dev)
 
         # ---- initial dictionary into the capacity slots
@@ -433,8 +432,8 @@ class FitEngine:
                     P(self.d_dict_off), P(self.d_m_cur), P(self.d_w_off), P(self.d_tile_mask),
                     P(self.d_col_off), P(self.d_W), P(self.d_lam1), P(self.d_lam2), P(self.d_tol),
                     P(self.d_max_iters), P(self.d_active), self.max_rows, P(self.d_beta),
-                    P(self.d_col_sq), P(self.d_sweeps), P(self.d_conv), P(self.d_obj), None, None,
-                    P(self.d_pair_dot), st), "pam_cd_tiles_f64")
+                    P(self.d_col_sq), P(self.d_sweeps), P(self.d_conv), P(self.d_obj), None, None, st),
+                    "pam_cd_tiles_f64")
             else:
                 nat.check(lib.pam_cd_f64(
                     len(order), P(d_order), P(self.d_row_off), P(self.d_y), P(self.d_dict_off),

@@ -238,6 +238,32 @@ def persistence_case():
     print("  persistence fixtures written")
 
 
+def c1_convergent_case():
+    """C1 with the library's convergent solver settings (tol=1e-10, max_iters=1e5; SURVEY
+    Appendix A): the reference's own fit() on each subdomain's lattice design matrix."""
+    wl = workloads.config1()
+    mesh = wl.field.mesh
+    boxes, _, _ = O.partition_boxes(mesh.counts, mesh.bounds, wl.shape)
+    e = wl.config.elastic
+    cfg = REN(lam1=e.lam1, lam2=e.lam2, tol=1e-10, max_iters=100000)
+    out = {"input_digest": digest(wl.field.values), "tol": 1e-10, "max_iters": 100000}
+    for s in range(len(boxes)):
+        lo, hi, _ = boxes[s]
+        rows = O.subdomain_rows(mesh.centroids, boxes[s])
+        d0 = RDict(centers=O.lattice_centers(lo, hi, wl.spec.lattice),
+                   widths=np.full(wl.spec.lattice ** mesh.dim, wl.spec.sigma))
+        W = r_features(mesh.centroids[rows], d0)
+        t = time.time()
+        res = r_fit(W, np.log(wl.field.values[rows]), cfg)
+        out[f"s{s}_beta"] = res.beta
+        out[f"s{s}_iterations"] = res.iterations
+        out[f"s{s}_converged"] = res.converged
+        out[f"s{s}_objective"] = res.objective
+        print(f"  C1conv subdomain {s}: {res.iterations} sweeps, converged={res.converged} "
+              f"({time.time() - t:.1f}s)", flush=True)
+    np.savez_compressed(OUT / "C1conv.npz", **out)
+
+
 def main(which):
     if "persistence" in which:
         persistence_case()
@@ -250,6 +276,8 @@ def main(which):
     if "C1" in which:
         wl = workloads.config1()
         save_case("C1", wl.field, wl.shape, [0, 1, 2, 3], wl.config, wl.spec)
+    if "C1conv" in which:
+        c1_convergent_case()
     if "C2" in which:
         wl = workloads.config2()
         save_case("C2", wl.field, wl.shape, [19, 42], wl.config, wl.spec)

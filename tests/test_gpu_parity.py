@@ -235,13 +235,12 @@ def test_tile_packed_stream_matches_dense(cuda, monkeypatch, cells):
 
 
 @pytest.mark.parametrize("variant", [{"PAM_CD_RING": "1"}, {"PAM_CD_LEAN": "0", "PAM_CD_COPY": "ldgsts"},
-                                     {"PAM_CD_LEAN": "0"}, {"PAM_CD_PAIR": "1"},
-                                     {"PAM_CD_LEAN": "3"}, {"PAM_TILE_RUNS": "2"},
-                                     {"PAM_TILE_RUNS": "0"}])
+                                     {"PAM_CD_LEAN": "0"}, {"PAM_CD_LEAN": "3"}, {"PAM_TILE_RUNS": "2"},
+                                     {"PAM_TILE_RUNS": "0"}, {"PAM_CD_STAGES": "4"}])
 def test_cd_staging_variants_match(cuda, monkeypatch, variant):
-    """Opt-in CD variants (byte ring, LDGSTS staging, generic tile kernel, column-pair
-    kernel, per-lane cp.async staging, two-run / exact tile masks) reproduce the default
-    single-column lean kernel."""
+    """Opt-in CD variants (byte ring, LDGSTS staging, generic tile kernel, per-lane
+    cp.async staging, two-run / exact tile masks, 4-slot ring) reproduce the default
+    lean kernel."""
     field = pam.box_field_2d(40, 40)
     part = pam.make_partition(field.mesh, 2, 2)  # 400 rows: the R=16 tile kernels
     cfg = pam.AdaptiveConfig(k_top=40, m_max=240, m_q=3, max_rounds=3, elastic=EN_2D,
@@ -362,21 +361,43 @@ def test_sharded_fit_single_rank_device_path(cuda):
 
 
 @pytest.mark.parametrize("cells", [(20, 20), (30, 30)])
-def test_pair_kernel_odd_column_counts(cuda, monkeypatch, cells):
-    """Column-pair CD (opt-in) with odd dictionary sizes (unpaired tail column) == single-column CD."""
+def test_lean_kernel_small_rows_odd_columns(cuda, monkeypatch, cells):
+    """Lean CD at R=4 / R=8 with odd dictionary sizes and ragged batches == the generic kernel."""
     field = pam.box_field_2d(*cells)
-    part = pam.make_partition(field.mesh, 2, 2)  # 100 / 225 rows: the R=4 / R=8 pair kernels
+    part = pam.make_partition(field.mesh, 2, 2)  # 100 / 225 rows
     cfg = pam.AdaptiveConfig(k_top=7, m_max=60, m_q=3, max_rounds=3, elastic=EN_2D,
                              offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
     spec = pam.DictionarySpec(sigma=0.5 / cells[0])
-    single, rs = pam.fit_parallel(field, part, cfg, spec)
-    monkeypatch.setenv("PAM_CD_PAIR", "1")
-    pair, rp = pam.fit_parallel(field, part, cfg, spec)
-    assert any(r.centers % 2 for reps in rp.rounds for r in reps)  # odd M was exercised
-    for a, b in zip(single.locals, pair.locals):
+    lean, rl = pam.fit_parallel(field, part, cfg, spec)
+    assert any(r.centers % 2 for reps in rl.rounds for r in reps)  # odd M was exercised
+    monkeypatch.setenv("PAM_CD_LEAN", "0")
+    gen, rg = pam.fit_parallel(field, part, cfg, spec)
+    for a, b in zip(gen.locals, lean.locals):
         np.testing.assert_array_equal(a.dictionary.centers, b.dictionary.centers)
         assert np.max(np.abs(a.beta - b.beta)) <= 1e-10 * max(1, np.abs(a.beta).max())
-    for ra, rb in zip(rs.rounds, rp.rounds):
+    for ra, rb in zip(rg.rounds, rl.rounds):
         for x, y in zip(ra, rb):
             assert (x.centers, x.added) == (y.centers, y.added)
             assert abs(x.objective - y.objective) <= 1e-10 * abs(x.objective)
+
+
+def test_config1_convergent_solver_matches_reference(cuda, golden):
+    """C1 with the library's convergent settings (tol=1e-10, max_iters=1e5):
+    every fit converges like the reference's (24,556 sweeps on the step subdomains),
+    beta and objective within 1e-8 relative, total sweeps within +-1 per fit."""
+    import dataclasses
+
+    g = golden("C1conv")
+    wl = workloads.config1()
+    assert str(g["input_digest"]) == __import__("hashlib").sha256(
+        np.ascontiguousarray(wl.field.values).tobytes()).hexdigest()
+    cfg = dataclasses.replace(wl.config, elastic=dataclasses.replace(wl.config.elastic, tol=1e-10,
+                                                                     max_iters=100000))
+    sur, rep = pam.fit_parallel(wl.field, wl.partition, cfg, wl.spec)
+    ref_sweeps = sum(int(g[f"s{s}_iterations"]) for s in range(4))
+    assert abs(rep.device["sweeps"] - ref_sweeps) <= 4
+    for s in range(4):
+        ref = g[f"s{s}_beta"]
+        assert np.max(np.abs(sur.locals[s].beta - ref)) <= 1e-8 * max(1.0, np.abs(ref).max())
+        obj = rep.rounds[s][0].objective
+        assert abs(obj - float(g[f"s{s}_objective"])) <= 1e-8 * max(abs(float(g[f"s{s}_objective"])), 1e-300)

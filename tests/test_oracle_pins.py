@@ -202,3 +202,21 @@ def test_3d_restatement_axis_consistency():
     part = partition.make_partition(mesh, *shape)
     np.testing.assert_array_equal(part.cell_to_subdomain, owner)
     assert part.grid is not None and part.is_cell_aligned()
+
+
+def test_config1_convergent_oracle_bit_exact(golden):
+    """The C oracle reproduces the reference's convergent C1 fits (tol=1e-10) bit for bit."""
+    g = golden("C1conv")
+    wl = workloads.config1()
+    mesh = wl.field.mesh
+    boxes, _, _ = O.partition_boxes(mesh.counts, mesh.bounds, wl.shape)
+    e = wl.config.elastic
+    for s in (0, 1):
+        lo, hi, _ = boxes[s]
+        rows = O.subdomain_rows(mesh.centroids, boxes[s])
+        c = O.lattice_centers(lo, hi, wl.spec.lattice)
+        W = O.shepard_features(mesh.centroids[rows], c, np.full(len(c), wl.spec.sigma))
+        res = O.fit(W, np.log(wl.field.values[rows]), e.lam1, e.lam2, 1e-10, 100000)
+        np.testing.assert_array_equal(res["beta"], g[f"s{s}_beta"])
+        assert res["iterations"] == int(g[f"s{s}_iterations"])
+        assert bool(res["converged"]) == bool(g[f"s{s}_converged"])
