@@ -133,8 +133,8 @@ eval_kernel(int64_t P, const double* __restrict__ pts, const int64_t* __restrict
     const int64_t s = sorted_owner[cur];  // block-uniform
     const bool live = have && my_owner == s;
     double den;
-    const double v = shepard_eval_block<D>(sm, x, live, centres, widths, beta, dict_off[s],
-                                           m_cur[s], &den);
+    const double v = shepard_eval_direct<D>(sm, x, live, centres, widths, beta, dict_off[s],
+                                            m_cur[s], &den);
     if (live) {
       if (shepard_degenerate(den)) report_error(err, PAM_ERR_DEGENERATE, j);
       out[j] = log_flag[s] ? exp(v) : v;

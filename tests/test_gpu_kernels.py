@@ -202,3 +202,23 @@ def test_locate_general_bounds_edges(cuda):
     owner = pam.locate_many(pts, part.boxes)
     ref = O.locate_many(pts, [(b.lo, b.hi, b.open_hi) for b in part.boxes])
     np.testing.assert_array_equal(owner, ref)
+
+
+def test_global_eval_underflow_rows_fall_back_exactly(cuda):
+    """K4's one-pass exp(L) sums underflow for points ~40 widths from every entry; those
+    rows are recomputed with the max-shifted two-pass form (rbf.py:152-167) and still match."""
+    mesh = pam.build_mesh(2, (8, 8), ((0.0, 1.0), (0.0, 1.0)))
+    part = pam.make_partition(mesh, 2, 2)
+    rng = np.random.default_rng(11)
+    locs, olocs = [], []
+    for b in part.boxes:
+        c = np.asarray(b.lo) + 0.05 + rng.random((6, 2)) * 0.05  # centres in one corner
+        w = np.full(6, 0.004)  # far corner of the box is > 80 widths away
+        beta = rng.standard_normal(6)
+        locs.append(pam.LocalSurrogate(dictionary=pam.RbfDictionary(centers=c, widths=w), beta=beta))
+        olocs.append((c, w, beta))
+    sur = pam.GlobalSurrogate(partition=part, locals=tuple(locs))
+    pts = rng.random((4000, 2))
+    ref, _ = O.global_evaluate(pts, [(b.lo, b.hi, b.open_hi) for b in part.boxes], olocs)
+    assert np.isfinite(ref).all()
+    np.testing.assert_allclose(sur.evaluate(pts), ref, rtol=1e-10)
