@@ -279,6 +279,29 @@ int pam_shepard_eval_host_f64(int dim, int64_t P, const double* pts, int64_t M,
 int64_t pam_format_entries_host(int dim, int64_t n, const double* centres, const double* widths,
                                 const double* beta, const int64_t* gens, char* out, int64_t cap);
 
+/* ---- Darcy consumer (reference darcy.py:238-375) -------
+ * pam_p1_values_f64: CSR values of the P1 stiffness matrix (darcy.py:308-346
+ * dim 2, 349-375 dim 1).  slot_ptr (nnz+1) / contrib list, per nonzero, the
+ * element contributions c = e*9 + 3i + j (dim 2) or e*4 + 2i + j (dim 1) in
+ * the reference's COO order; values are summed in that order (bit-identical
+ * to its COO -> CSR sum).  elem_nodes (n_elem, dim+1), nodes (n_nodes, dim),
+ * coef (n_elem) = coefficient at element centroids (validated by the caller).
+ * pam_csr_spmv_f64: y = A x.
+ * pam_pcg_f64: scipy.sparse.linalg.cg with M = diag(1/a_ii) (1 where
+ * a_ii <= 0), x0 = 0, stop when ||r|| < rtol ||b|| (darcy.py:275-289); work
+ * = pam_pcg_workspace_bytes(n) bytes of device memory.  Returns the completed
+ * iterations, converged (0 = max_iter reached) and the recursive residual
+ * ratio; fixed-order reductions (deterministic). */
+int pam_p1_values_f64(int dim, int64_t nnz, const int64_t* slot_ptr, const int64_t* contrib,
+                      const int64_t* elem_nodes, const double* nodes, const double* coef,
+                      double* values, void* stream);
+int pam_csr_spmv_f64(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,
+                     const double* x, double* y, void* stream);
+int64_t pam_pcg_workspace_bytes(int64_t n);
+int pam_pcg_f64(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,
+                const double* b, double* x, double rtol, int64_t max_iter, void* work,
+                int64_t* iterations, int32_t* converged, double* rel_residual, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -146,7 +146,8 @@ eval_kernel(int64_t P, const double* __restrict__ pts, const int64_t* __restrict
   }
 }
 
-// single-dictionary Shepard evaluation (rbf.py:152-167 / 190-192)
+// single-dictionary Shepard evaluation (rbf.py:152-167 / 190-192); same
+// arithmetic as eval_kernel, so LocalSurrogate and GlobalSurrogate agree bit for bit
 template <int D>
 __global__ void __launch_bounds__(EVAL_TILE)
 shepard_single_kernel(int64_t P, const double* __restrict__ pts, int M,
@@ -160,7 +161,7 @@ shepard_single_kernel(int64_t P, const double* __restrict__ pts, int M,
 #pragma unroll
   for (int k = 0; k < D; ++k) x[k] = live ? pts[j * D + k] : 0.0;
   double den;
-  const double v = shepard_eval_block<D>(sm, x, live, centres, widths, beta, 0, M, &den);
+  const double v = shepard_eval_direct<D>(sm, x, live, centres, widths, beta, 0, M, &den);
   if (live) {
     if (shepard_degenerate(den)) report_error(err, PAM_ERR_DEGENERATE, j);
     out[j] = exp_out ? exp(v) : v;

@@ -264,6 +264,51 @@ def c1_convergent_case():
     np.savez_compressed(OUT / "C1conv.npz", **out)
 
 
+def darcy_case():
+    """The reference's P1 Darcy solver on four problems (direct and CG paths, holes, Neumann,
+    source, 1D, and a fitted surrogate as the coefficient)."""
+    from fieldfit import darcy as rd
+
+    out = {}
+    coef = lambda p: np.exp(np.sin(3 * p[:, 0]) * np.cos(2 * p[:, 1]))  # noqa: E731
+    cases = {
+        "d1": rd.DarcyProblem(mesh=rd.triangulate(40, 30, ((0.0, 2.0), (0.0, 1.0))), coefficient=coef,
+                              dirichlet={"left": 1.0, "right": 0.0}),
+        "d2": rd.DarcyProblem(mesh=rd.triangulate(160, 140, ((0.0, 1.0), (0.0, 1.0)), holes=[(0.5, 0.5, 0.12)]),
+                              coefficient=lambda p: 10.0 ** (np.where(p[:, 0] > 0.3, 1.0, -0.5)
+                                                            + 0.3 * np.sin(7 * p[:, 1])),
+                              dirichlet={"left": lambda p: 1.0 + p[:, 1], "right": 0.0},
+                              neumann={"top": 0.3}, source=1.0),
+        "d3": rd.DarcyProblem(mesh=rd.line_mesh(50, (0.0, 2.0)), coefficient=lambda p: np.exp(p[:, 0]),
+                              dirichlet={"left": 1.0}, neumann={"right": 0.5}, source=2.0),
+    }
+    field = ff.box_field_2d(16, 16)
+    part = ff.make_partition(field.mesh, 2, 2)
+    sur, _ = ff.fit_parallel(field, part, ff.AdaptiveConfig(
+        k_top=12, m_max=72, m_q=3, max_rounds=2, offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)),
+        elastic=REN(lam1=4.59e-4, lam2=1e-4, tol=1e-6, max_iters=400)), ff.DictionarySpec(sigma=0.0625))
+    import io as _io
+    buf = _io.StringIO()
+    ff.save(sur, buf)
+    out["d4_surrogate"] = np.array(buf.getvalue())
+    cases["d4"] = rd.DarcyProblem(mesh=rd.triangulate(30, 30, ((0.0, 1.0), (0.0, 1.0))),
+                                  coefficient=sur.evaluate, dirichlet={"bottom": 0.0, "top": 1.0})
+    for name, prob in cases.items():
+        sol = rd.solve_darcy(prob)
+        A, b = sol.system
+        A = A.tocsr()
+        A.sort_indices()
+        out[f"{name}_values"] = sol.values
+        out[f"{name}_iterations"] = sol.diagnostics["iterations"]
+        out[f"{name}_method"] = np.array(sol.diagnostics["method"])
+        out[f"{name}_A_data"], out[f"{name}_A_indices"], out[f"{name}_A_indptr"] = A.data, A.indices, A.indptr
+        out[f"{name}_b"] = b
+        if prob.mesh.dim == 2:
+            out[f"{name}_reaction_left"] = sol.boundary_reaction(list(prob.dirichlet)[0])
+        print(f"  darcy {name}: {sol.diagnostics}", flush=True)
+    np.savez_compressed(OUT / "darcy.npz", **out)
+
+
 def main(which):
     if "persistence" in which:
         persistence_case()
@@ -276,6 +321,8 @@ def main(which):
     if "C1" in which:
         wl = workloads.config1()
         save_case("C1", wl.field, wl.shape, [0, 1, 2, 3], wl.config, wl.spec)
+    if "darcy" in which:
+        darcy_case()
     if "C1conv" in which:
         c1_convergent_case()
     if "C2" in which:
