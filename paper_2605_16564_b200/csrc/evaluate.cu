@@ -10,20 +10,20 @@
 //      edges, so ownership is bit-exact.  Points outside every
 //      box report the FIRST offending index (atomicMin).
 //   2. counting sort of point ids by owner (histogram, exclusive scan,
-//      scatter) so each subdomain's dictionary is read from HBM once per
-//      128-point tile and served to the tile from shared memory.
-//   3. eval: per tile, per owner run, the two-pass Shepard sum with the
-//      dictionary staged in smem; exp() of the blend when log_transform;
-//      results scattered back to input order.
+//      scatter) so each subdomain's dictionary is read once per 64-point
+//      warp tile (from L2) and served to the warp from shared memory.
+//   3. eval: one warp per 64 sorted points, per owner run the one-pass
+//      Shepard sum with a table-driven FP64 exp (below); exp() of the blend
+//      when log_transform; results scattered back to input order.
 //
 // Roofline: FP64-pipe bound (M*(3d+4+E) flops per point vs 8d+8 bytes).
 #include "shepard.cuh"
 
+#include <string.h>
+
 #include <algorithm>
 
 namespace pam {
-
-constexpr int EVAL_TILE = 128;
 
 template <int D>
 __global__ void locate_kernel(int64_t P, const double* __restrict__ pts,
@@ -111,61 +111,322 @@ __global__ void scatter_kernel(int64_t P, const int64_t* __restrict__ owner,
   }
 }
 
+// ----------------------------------------------------------------------------
+// K4 evaluation kernel: one WARP per 32*PT consecutive owner-sorted points
+// (PT points per lane), no block-wide barriers.  For each owner run inside the
+// warp the owner's dictionary is streamed 32 entries at a time: lane l loads
+// entry j0+l, converts it to (centre, g = K/(2w^2), beta) in a per-warp shared
+// block, and every lane then reads the entries as broadcasts and accumulates
+// its PT points (register blocking: one staged entry feeds PT points).
+//
+// exp() of the (<= 0) log-feature uses a table-driven FP64 exponential that
+// spends 11 FP64 instructions instead of libdevice's ~20 (the FP64 pipe is the
+// binding roofline):
+//   t = -g * d^2 = L * 2048/ln2 with g = K/(2w^2), K = 2048/ln2,
+//   n = rint(t) by the 1.5*2^52 shift (one DFMA), f = t - n in [-1/2, 1/2]
+//   exactly rounded by one DFMA, 2^(f/2048) by a degree-3 polynomial
+//   (truncation <= 3.4e-17 relative), 2^(n/2048) = 2^(n>>11) * T[n & 2047]
+//   with T in shared memory and 2^(n>>11) added into T's exponent field by an
+//   integer add (no FP64 op).  Terms below 2^-1022 are flushed to 0; a point
+//   whose every term underflows (den < 1e-280, ~27 widths from all entries) is
+//   redone with the reference's exact max-shifted two-pass form.
+// Per-term relative error ~1e-16*(1+|L|), the same order as the reference's
+// own rounding of L (rbf.py:87-90); values agree with the oracle to ~1e-14.
+
+constexpr int XT_BITS = 11;
+constexpr int XT = 1 << XT_BITS;
+constexpr int EVAL_WARPS = 8;  // warps per CTA
+constexpr double EXP_K = 2954.639443740597;   // 2048 / ln 2
+constexpr double EXP_C1 = 3.384507717577858e-04;   // ln2/2048 (exact scaling of ln2)
+constexpr double EXP_C2 = 5.72744624517204e-08;    // (ln2/2048)^2 / 2
+constexpr double EXP_C3 = 6.461528672932365e-12;   // (ln2/2048)^3 / 6
+constexpr double EXP_SHIFT = 6755399441055744.0;   // 1.5 * 2^52
+constexpr long long EXP_SHIFT_BITS = 0x4338000000000000LL;
+constexpr long long EXP_NMIN = -1022LL * XT;        // 2^(n/2048) >= 2^-1022
+
+// table word j: the bits of 2^(j/2048) with (j << 9) subtracted from the high
+// word, so hi + (n << 9) == hi(2^(j/2048)) + ((n >> 11) << 20) for
+// n = 2048 (n >> 11) + j: one integer multiply-add applies the 2^(n >> 11)
+// scale (see ensure_exp2_table)
+__device__ unsigned long long g_exp2_table[XT];
+__device__ unsigned long long g_eval_queue;
+
+// exp(-g * d2) with g = K/(2 w^2) -- see the block comment above
+__device__ __forceinline__ double exp_neg_scaled(double d2, double g, const unsigned long long* tab) {
+  const double s = fma(d2, -g, EXP_SHIFT);
+  const double nd = s - EXP_SHIFT;
+  const double f = fma(-g, d2, -nd);
+  const long long sb = __double_as_longlong(s);
+  const unsigned lo = static_cast<unsigned>(sb);
+  const unsigned long long tw = tab[lo & (XT - 1)];
+  const unsigned hi = static_cast<unsigned>(tw >> 32) + (lo << 9);
+  // below 2^-1022 only the high word is cleared: the term becomes a denormal
+  // < 2^-1022 (relative effect < 1e-25 on any denominator >= 1e-280)
+  const double Ts = __hiloint2double(static_cast<int>((sb >= EXP_SHIFT_BITS + EXP_NMIN) ? hi : 0u),
+                                     static_cast<int>(static_cast<unsigned>(tw)));
+  const double p = fma(f, fma(f, fma(f, EXP_C3, EXP_C2), EXP_C1), 1.0);
+  return Ts * p;
+}
+
+// Variant R (PAM_EVAL_TAB=256): a 256-entry table replicated 16 times so a
+// warp's random table reads hit at most 2 shared-memory wavefronts (the 2048
+// table averages ~5), paid for by a degree-4 polynomial (one more DFMA).
+constexpr int XR_BITS = 8;
+constexpr int XR = 1 << XR_BITS;
+constexpr int XR_REP = 16;
+constexpr double EXR_K = 369.3299304675746;        // 256 / ln 2
+constexpr double EXR_C1 = 0.0027076061740622863;   // ln2/256
+constexpr double EXR_C2 = 3.665565596910106e-06;
+constexpr double EXR_C3 = 3.308302680541371e-09;
+constexpr double EXR_C4 = 2.239395190875157e-12;
+constexpr long long EXR_NMIN = -1022LL * XR;
+__device__ unsigned long long g_exp2_table_r[XR];
+
+__device__ __forceinline__ double exp_neg_scaled_r(double d2, double g, const unsigned long long* tab,
+                                                   int rep) {
+  const double s = fma(d2, -g, EXP_SHIFT);
+  const double nd = s - EXP_SHIFT;
+  const double f = fma(-g, d2, -nd);
+  const long long sb = __double_as_longlong(s);
+  const unsigned lo = static_cast<unsigned>(sb);
+  const unsigned long long tw = tab[((lo & (XR - 1)) * XR_REP) + rep];
+  const unsigned hi = static_cast<unsigned>(tw >> 32) + (lo << (20 - XR_BITS));
+  const double Ts = __hiloint2double(static_cast<int>((sb >= EXP_SHIFT_BITS + EXR_NMIN) ? hi : 0u),
+                                     static_cast<int>(static_cast<unsigned>(tw)));
+  const double p = fma(f, fma(f, fma(f, fma(f, EXR_C4, EXR_C3), EXR_C2), EXR_C1), 1.0);
+  return Ts * p;
+}
+
+// the reference's exact max-shifted two-pass Shepard sum (rbf.py:152-167) for
+// one point, reading the dictionary from global memory (underflow fallback)
 template <int D>
-__global__ void __launch_bounds__(EVAL_TILE)
+__device__ double shepard_exact_point(const double* x, const double* centres, const double* widths,
+                                      const double* beta, int64_t doff, int M, double* den_out) {
+  double mx = -INFINITY;
+  for (int t = 0; t < M; ++t) {
+    double c[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) c[k] = centres[(doff + t) * D + k];
+    mx = fmax(mx, log_feature<D>(x, c, inv_two_sigma_sq(widths[doff + t])));
+  }
+  double num = 0.0, den = 0.0;
+  for (int t = 0; t < M; ++t) {
+    double c[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) c[k] = centres[(doff + t) * D + k];
+    const double e = exp(__dsub_rn(log_feature<D>(x, c, inv_two_sigma_sq(widths[doff + t])), mx));
+    num = fma(e, beta[doff + t], num);
+    den = __dadd_rn(den, e);
+  }
+  *den_out = den;
+  return num / den;
+}
+
+// sorted_owner == nullptr: single-dictionary mode (LocalSurrogate.evaluate /
+// shepard_eval, rbf.py:152-192): every point belongs to dictionary 0 of
+// size single_m, log transform = single_exp.  perm == nullptr: identity.
+template <int D, int PT, bool REPL>
+__global__ void __launch_bounds__(EVAL_WARPS * 32)
 eval_kernel(int64_t P, const double* __restrict__ pts, const int64_t* __restrict__ perm,
             const int64_t* __restrict__ sorted_owner, const int64_t* __restrict__ dict_off,
             const int32_t* __restrict__ m_cur, const double* __restrict__ centres,
             const double* __restrict__ widths, const double* __restrict__ beta,
-            const int32_t* __restrict__ log_flag, double* __restrict__ out, int64_t* err) {
-  __shared__ ShepardSmem<D> sm;
-  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * EVAL_TILE;
-  const int64_t tend = min(P, t0 + EVAL_TILE);
-  const int64_t mine = t0 + threadIdx.x;
-  const bool have = mine < tend;
-  const int64_t my_owner = have ? sorted_owner[mine] : -1;
-  const int64_t j = have ? perm[mine] : 0;
-  double x[D];
+            const int32_t* __restrict__ log_flag, int single_m, int single_exp,
+            double* __restrict__ out, int64_t* err) {
+  constexpr int REC = (D + 2 + 1) & ~1;  // staged record: centre, g, beta (16-byte aligned)
+  constexpr int TAB = REPL ? XR * XR_REP : XT;
+  __shared__ unsigned long long tab[TAB];
+  __shared__ __align__(16) double stage[EVAL_WARPS][32 * REC];
+  for (int i = threadIdx.x; i < TAB; i += blockDim.x)
+    tab[i] = REPL ? g_exp2_table_r[i / XR_REP] : g_exp2_table[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int rep = lane & (XR_REP - 1);
+  double* const st = stage[warp];
+  const int64_t n_tiles = (P + 32 * PT - 1) / (32 * PT);
+  // persistent warps pulling 32*PT-point tiles from a global queue: balanced
+  // whatever the owner-run mix of a tile and however many CTAs are resident
+  while (true) {
+    unsigned long long tq = 0;
+    if (lane == 0) tq = atomicAdd(&g_eval_queue, 1ull);
+    const int64_t tile = static_cast<int64_t>(__shfl_sync(0xffffffffu, tq, 0));
+    if (tile >= n_tiles) break;
+    const int64_t base = tile * (32 * PT);
+    bool have[PT];
+    int64_t own[PT], idx[PT];
+    double x[PT][D];
 #pragma unroll
-  for (int k = 0; k < D; ++k) x[k] = have ? pts[j * D + k] : 0.0;
-  int64_t cur = t0;
-  while (cur < tend) {
-    const int64_t s = sorted_owner[cur];  // block-uniform
-    const bool live = have && my_owner == s;
-    double den;
-    const double v = shepard_eval_direct<D>(sm, x, live, centres, widths, beta, dict_off[s],
-                                            m_cur[s], &den);
-    if (live) {
-      if (shepard_degenerate(den)) report_error(err, PAM_ERR_DEGENERATE, j);
-      out[j] = log_flag[s] ? exp(v) : v;
+    for (int p = 0; p < PT; ++p) {
+      const int64_t pos = base + 32 * p + lane;
+      have[p] = pos < P;
+      own[p] = have[p] ? (sorted_owner ? sorted_owner[pos] : 0) : INT64_MAX;
+      idx[p] = have[p] ? (perm ? perm[pos] : pos) : 0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) x[p][k] = have[p] ? pts[idx[p] * D + k] : 0.0;
     }
-    // advance past this owner's run (sorted => contiguous)
-    int64_t nxt = cur;
-    while (nxt < tend && sorted_owner[nxt] == s) ++nxt;
-    cur = nxt;
+    // owners are nondecreasing along the sorted positions: lane 0's first
+    // point holds the tile's smallest owner
+    int64_t cur = __shfl_sync(0xffffffffu, own[0], 0);
+    while (true) {
+      const int64_t s = cur;
+      const int64_t doff = dict_off ? dict_off[s] : 0;
+      const int M = m_cur ? m_cur[s] : single_m;
+      double num[PT], den[PT];
+#pragma unroll
+      for (int p = 0; p < PT; ++p) num[p] = den[p] = 0.0;
+      for (int j0 = 0; j0 < M; j0 += 32) {
+        const int cnt = min(32, M - j0);
+        __syncwarp();
+        if (lane < cnt) {
+          const int64_t e = doff + j0 + lane;
+          double* r = st + lane * REC;
+#pragma unroll
+          for (int k = 0; k < D; ++k) r[k] = centres[e * D + k];
+          r[D] = __dmul_rn(inv_two_sigma_sq(widths[e]), REPL ? EXR_K : EXP_K);
+          r[D + 1] = beta[e];
+        }
+        __syncwarp();
+#pragma unroll 2
+        for (int t = 0; t < cnt; ++t) {
+          // broadcast 16-byte loads of the staged record
+          double rec[REC];
+#pragma unroll
+          for (int q = 0; q < REC / 2; ++q) {
+            const double2 v = reinterpret_cast<const double2*>(st + t * REC)[q];
+            rec[2 * q] = v.x;
+            rec[2 * q + 1] = v.y;
+          }
+          const double g = rec[D], b = rec[D + 1];
+#pragma unroll
+          for (int p = 0; p < PT; ++p) {
+            double d2 = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+              const double dk = x[p][k] - rec[k];
+              d2 = fma(dk, dk, d2);
+            }
+            const double e = REPL ? exp_neg_scaled_r(d2, g, tab, rep) : exp_neg_scaled(d2, g, tab);
+            num[p] = fma(e, b, num[p]);
+            den[p] += e;
+          }
+        }
+      }
+      const int lf = log_flag ? log_flag[s] : single_exp;
+#pragma unroll
+      for (int p = 0; p < PT; ++p) {
+        if (have[p] && own[p] == s) {
+          double dn = den[p], v;
+          if (dn >= 1e-280) {
+            v = num[p] / dn;
+          } else {
+            v = shepard_exact_point<D>(x[p], centres, widths, beta, doff, M, &dn);
+          }
+          if (shepard_degenerate(dn)) report_error(err, PAM_ERR_DEGENERATE, idx[p]);
+          out[idx[p]] = lf ? exp(v) : v;
+        }
+      }
+      // next owner present in this tile
+      int64_t nxt = INT64_MAX;
+#pragma unroll
+      for (int p = 0; p < PT; ++p)
+        if (own[p] > s && own[p] < nxt) nxt = own[p];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const int64_t other = __shfl_xor_sync(0xffffffffu, nxt, o);
+        nxt = other < nxt ? other : nxt;
+      }
+      if (nxt == INT64_MAX) break;
+      cur = nxt;
+    }
   }
 }
 
-// single-dictionary Shepard evaluation (rbf.py:152-167 / 190-192); same
-// arithmetic as eval_kernel, so LocalSurrogate and GlobalSurrogate agree bit for bit
-template <int D>
-__global__ void __launch_bounds__(EVAL_TILE)
-shepard_single_kernel(int64_t P, const double* __restrict__ pts, int M,
-                      const double* __restrict__ centres, const double* __restrict__ widths,
-                      const double* __restrict__ beta, int exp_out, double* __restrict__ out,
-                      int64_t* err) {
-  __shared__ ShepardSmem<D> sm;
-  const int64_t j = static_cast<int64_t>(blockIdx.x) * EVAL_TILE + threadIdx.x;
-  const bool live = j < P;
-  double x[D];
-#pragma unroll
-  for (int k = 0; k < D; ++k) x[k] = live ? pts[j * D + k] : 0.0;
-  double den;
-  const double v = shepard_eval_direct<D>(sm, x, live, centres, widths, beta, 0, M, &den);
-  if (live) {
-    if (shepard_degenerate(den)) report_error(err, PAM_ERR_DEGENERATE, j);
-    out[j] = exp_out ? exp(v) : v;
+// points per lane (register blocking, env PAM_EVAL_PT = 2 | 4, default 4) and
+// exp table (env PAM_EVAL_TAB = 2048 | 256, default 2048)
+int eval_pt() {
+  static int pt = [] {
+    const char* e = getenv("PAM_EVAL_PT");
+    return (e && atoi(e) == 2) ? 2 : 4;
+  }();
+  return pt;
+}
+bool eval_repl() {
+  static bool r = [] {
+    const char* e = getenv("PAM_EVAL_TAB");
+    return e && atoi(e) == 256;
+  }();
+  return r;
+}
+
+int ensure_exp2_table() {
+  static bool done = false;  // one GPU per process
+  if (done) return PAM_OK;
+  unsigned long long h[XT];
+  for (int j = 0; j < XT; ++j) {
+    const double t = static_cast<double>(exp2l(static_cast<long double>(j) / XT));
+    unsigned long long b;
+    memcpy(&b, &t, sizeof(b));
+    h[j] = b - (static_cast<unsigned long long>(static_cast<unsigned>(j) << 9) << 32);
   }
+  PAM_CUDA_CHECK(cudaMemcpyToSymbol(g_exp2_table, h, sizeof(h)));
+  unsigned long long hr[XR];
+  for (int j = 0; j < XR; ++j) {
+    const double t = static_cast<double>(exp2l(static_cast<long double>(j) / XR));
+    unsigned long long b;
+    memcpy(&b, &t, sizeof(b));
+    hr[j] = b - (static_cast<unsigned long long>(static_cast<unsigned>(j) << (20 - XR_BITS)) << 32);
+  }
+  PAM_CUDA_CHECK(cudaMemcpyToSymbol(g_exp2_table_r, hr, sizeof(hr)));
+  done = true;
+  return PAM_OK;
+}
+
+template <int D, int PT, bool REPL>
+int launch_eval_v(cudaStream_t st, int64_t P, const double* pts, const int64_t* perm,
+                  const int64_t* sorted_owner, const int64_t* dict_off, const int32_t* m_cur,
+                  const double* centres, const double* widths, const double* beta,
+                  const int32_t* log_flag, int single_m, int single_exp, double* out, int64_t* err) {
+  static int grid_cap = 0;
+  if (grid_cap == 0) {
+    int dev = 0, sms = 148, per_sm = 1;
+    PAM_CUDA_CHECK(cudaGetDevice(&dev));
+    PAM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    // maximum shared-memory carve-out, so the occupancy the grid is sized for
+    // is the one the SM actually grants
+    PAM_CUDA_CHECK(cudaFuncSetAttribute(eval_kernel<D, PT, REPL>,
+                                        cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    PAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eval_kernel<D, PT, REPL>,
+                                                                 EVAL_WARPS * 32, 0));
+    grid_cap = sms * std::max(per_sm, 1);
+  }
+  const int64_t ctas = std::min<int64_t>(grid_cap, ceil_div(P, static_cast<int64_t>(EVAL_WARPS) * 32 * PT));
+  void* qaddr = nullptr;
+  PAM_CUDA_CHECK(cudaGetSymbolAddress(&qaddr, g_eval_queue));
+  PAM_CUDA_CHECK(cudaMemsetAsync(qaddr, 0, sizeof(unsigned long long), st));
+  eval_kernel<D, PT, REPL><<<(unsigned)ctas, EVAL_WARPS * 32, 0, st>>>(
+      P, pts, perm, sorted_owner, dict_off, m_cur, centres, widths, beta, log_flag, single_m,
+      single_exp, out, err);
+  PAM_LAUNCH_CHECK("eval_kernel");
+  return PAM_OK;
+}
+
+template <int D>
+int launch_eval(cudaStream_t st, int64_t P, const double* pts, const int64_t* perm,
+                const int64_t* sorted_owner, const int64_t* dict_off, const int32_t* m_cur,
+                const double* centres, const double* widths, const double* beta,
+                const int32_t* log_flag, int single_m, int single_exp, double* out, int64_t* err) {
+  const int rc = ensure_exp2_table();
+  if (rc != PAM_OK) return rc;
+#define PAM_EVAL_ARGS st, P, pts, perm, sorted_owner, dict_off, m_cur, centres, widths, beta, log_flag, \
+                      single_m, single_exp, out, err
+  if (eval_pt() == 4) {
+    if (eval_repl()) return launch_eval_v<D, 4, true>(PAM_EVAL_ARGS);
+    return launch_eval_v<D, 4, false>(PAM_EVAL_ARGS);
+  }
+  if (eval_repl()) return launch_eval_v<D, 2, true>(PAM_EVAL_ARGS);
+  return launch_eval_v<D, 2, false>(PAM_EVAL_ARGS);
+#undef PAM_EVAL_ARGS
 }
 
 int grid_for(int64_t n, int threads) {
@@ -223,19 +484,14 @@ extern "C" int pam_eval_f64(int dim, int64_t P, const double* pts, const int32_t
   PAM_CUDA_CHECK(cudaMemsetAsync(perm, 0, P * sizeof(int64_t), st));
   scatter_kernel<<<g, 256, 0, st>>>(P, owner, cursor, perm, sorted_owner);
   PAM_LAUNCH_CHECK("scatter_kernel");
-  const int64_t tiles = ceil_div(P, EVAL_TILE);
-  if (tiles > 0x7fffffffLL) return PAM_ERR_ARG;
   if (dim == 1)
-    eval_kernel<1><<<(unsigned)tiles, EVAL_TILE, 0, st>>>(P, pts, perm, sorted_owner, dict_off, m_cur,
-                                                          centres, widths, beta, log_flag, out, err);
-  else if (dim == 2)
-    eval_kernel<2><<<(unsigned)tiles, EVAL_TILE, 0, st>>>(P, pts, perm, sorted_owner, dict_off, m_cur,
-                                                          centres, widths, beta, log_flag, out, err);
-  else
-    eval_kernel<3><<<(unsigned)tiles, EVAL_TILE, 0, st>>>(P, pts, perm, sorted_owner, dict_off, m_cur,
-                                                          centres, widths, beta, log_flag, out, err);
-  PAM_LAUNCH_CHECK("eval_kernel");
-  return PAM_OK;
+    return launch_eval<1>(st, P, pts, perm, sorted_owner, dict_off, m_cur, centres, widths, beta,
+                          log_flag, 0, 0, out, err);
+  if (dim == 2)
+    return launch_eval<2>(st, P, pts, perm, sorted_owner, dict_off, m_cur, centres, widths, beta,
+                          log_flag, 0, 0, out, err);
+  return launch_eval<3>(st, P, pts, perm, sorted_owner, dict_off, m_cur, centres, widths, beta,
+                        log_flag, 0, 0, out, err);
 }
 
 extern "C" int pam_shepard_eval_f64(int dim, int64_t P, const double* pts, int64_t M,
@@ -245,16 +501,13 @@ extern "C" int pam_shepard_eval_f64(int dim, int64_t P, const double* pts, int64
   if (dim < 1 || dim > 3 || P < 0 || M < 1 || M > 0x7fffffff) return PAM_ERR_ARG;
   if (P == 0) return PAM_OK;
   cudaStream_t st = as_stream(stream);
-  const int64_t tiles = ceil_div(P, EVAL_TILE);
+  const int m = static_cast<int>(M);
   if (dim == 1)
-    shepard_single_kernel<1><<<(unsigned)tiles, EVAL_TILE, 0, st>>>(P, pts, (int)M, centres, widths,
-                                                                    beta, exp_out, out, err);
-  else if (dim == 2)
-    shepard_single_kernel<2><<<(unsigned)tiles, EVAL_TILE, 0, st>>>(P, pts, (int)M, centres, widths,
-                                                                    beta, exp_out, out, err);
-  else
-    shepard_single_kernel<3><<<(unsigned)tiles, EVAL_TILE, 0, st>>>(P, pts, (int)M, centres, widths,
-                                                                    beta, exp_out, out, err);
-  PAM_LAUNCH_CHECK("shepard_single_kernel");
-  return PAM_OK;
+    return launch_eval<1>(st, P, pts, nullptr, nullptr, nullptr, nullptr, centres, widths, beta,
+                          nullptr, m, exp_out, out, err);
+  if (dim == 2)
+    return launch_eval<2>(st, P, pts, nullptr, nullptr, nullptr, nullptr, centres, widths, beta,
+                          nullptr, m, exp_out, out, err);
+  return launch_eval<3>(st, P, pts, nullptr, nullptr, nullptr, nullptr, centres, widths, beta,
+                        nullptr, m, exp_out, out, err);
 }

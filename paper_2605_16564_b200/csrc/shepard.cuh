@@ -65,53 +65,6 @@ __device__ double shepard_eval_block(ShepardSmem<D>& sm, const double* x, bool l
   return num / den;
 }
 
-// Global-evaluation variant (K4 only; the residual kernel keeps the two-pass
-// form above because its values feed the tie-sensitive marking): one pass with
-// the shift 0 instead of the row maximum.  L <= 0 always, so exp(L) cannot
-// overflow; the ratio sum(beta e^L) / sum(e^L) equals the reference's
-// max-shifted ratio up to rounding (~1e-16 relative).  Only when every
-// exp(L) underflows (a point ~27 widths from all entries) is the row redone
-// with the exact two-pass form.  Distances use FMA (no tie decision here).
-template <int D>
-__device__ __forceinline__ double log_feature_fast(const double* x, const double* c, double inv) {
-  double acc = 0.0;
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    const double d = x[k] - c[k];
-    acc = fma(d, d, acc);
-  }
-  return -acc * inv;
-}
-
-template <int D>
-__device__ double shepard_eval_direct(ShepardSmem<D>& sm, const double* x, bool live,
-                                      const double* centres, const double* widths,
-                                      const double* beta, int64_t doff, int M, double* den_out) {
-  double num = 0.0, den = 0.0;
-  for (int j0 = 0; j0 < M; j0 += SH_CHUNK) {
-    const int cnt = min(SH_CHUNK, M - j0);
-    stage_dict<D>(sm, centres, widths, beta, doff, j0, cnt);
-    if (live)
-      for (int t = 0; t < cnt; ++t) {
-        const double e = exp(log_feature_fast<D>(x, &sm.c[t * D], sm.inv[t]));
-        num = fma(e, sm.beta[t], num);
-        den += e;
-      }
-  }
-  // block-uniform fallback: any live row whose sum underflowed reruns exactly
-  const int redo = __syncthreads_or(live && !(den >= 1e-280));
-  if (redo) {
-    double den2 = 0.0;
-    const double v = shepard_eval_block<D>(sm, x, live, centres, widths, beta, doff, M, &den2);
-    if (live && !(den >= 1e-280)) {
-      *den_out = den2;
-      return v;
-    }
-  }
-  *den_out = den;
-  return num / den;
-}
-
 __device__ __forceinline__ bool shepard_degenerate(double den) {
   return !isfinite(den) || den <= 0.0;
 }
