@@ -14,11 +14,13 @@
 //     the CD kernel fetches a column with ONE cp.async.bulk of
 //     popcount(mask) * 256 bytes.
 //
-// Entries below tau are dropped.  With the default tau = 2^-100 (~7.9e-31)
-// a dropped entry changes a CD dot product z_j = sum_i W_ij r_i by at most
-// tau * sum_i |r_i|, ~15 orders of magnitude below the FP64 rounding of the
-// dot itself, so results are unchanged at any tolerance the reference can
-// resolve; tau = 0 keeps every tile (exact dense streaming, K1 semantics).
+// Entries below tau are dropped.  A dropped entry changes a CD dot product
+// z_j = sum_i W_ij r_i by at most tau * sum_i |r_i|.  The default tau = 1e-16
+// is below the FP64 unit roundoff of a row of W (rows sum to 1): zeroing every
+// entry below it moves the reference's adaptive fits by ~1e-13 relative
+// (tests/test_oracle_pins.py), five orders below the parity tolerance;
+// tau = 2^-100 drops only entries invisible to FP64 sums, tau = 0 keeps every
+// tile (exact dense streaming, K1 semantics).
 //
 // Three launches: (A) row max/sum + tile masks (ballot per warp = per tile),
 // (B) per-subdomain exclusive scan of popcounts -> col_off, (C) packed store.

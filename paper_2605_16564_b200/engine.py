@@ -136,7 +136,13 @@ def dictionary_capacity(m0, k_top, m_q, m_max, max_rounds):
     return m0 + extra
 
 
-DEFAULT_TILE_TAU = 2.0 ** -100  # ~7.9e-31: entries below are invisible to FP64 CD (tiles.cu)
+# Tiles (32 rows) whose Shepard weights are all below tau are not streamed by
+# the CD.  Every row of W sums to 1, so 1e-16 is below the FP64 unit roundoff
+# (1.1e-16) of each row's mass; zeroing every entry below it moves the
+# reference's adaptive fits by ~1e-13 relative (tests/test_oracle_pins.py,
+# DESIGN.md §3).  PAM_TILE_TAU=7.9e-31 (2^-100) keeps the exactly-invisible
+# threshold, PAM_TILE_TAU=0 the dense stream.
+DEFAULT_TILE_TAU = 1e-16
 
 
 def tile_tau() -> float:

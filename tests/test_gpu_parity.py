@@ -212,9 +212,11 @@ def test_fit_parallel_deterministic_and_chunk_independent(cuda, monkeypatch):
     assert pam.dumps(s1) == pam.dumps(s4)
 
 
+@pytest.mark.parametrize("tau", [2.0 ** -100, 1e-16])
 @pytest.mark.parametrize("cells", [(16, 16), (40, 40)])
-def test_tile_packed_stream_matches_dense(cuda, monkeypatch, cells):
-    """Tile-dropping (tau = 2^-100) vs exact dense streaming: same decisions, beta ~1e-12."""
+def test_tile_packed_stream_matches_dense(cuda, monkeypatch, cells, tau):
+    """Tile-dropping (tau = 2^-100 and the default 1e-16) vs exact dense streaming:
+    same decisions, beta ~1e-12."""
     field = pam.box_field_2d(*cells)
     part = pam.make_partition(field.mesh, 2, 2)
     cfg = pam.AdaptiveConfig(k_top=cells[0], m_max=6 * cells[0], m_q=3, max_rounds=3, elastic=EN_2D,
@@ -222,7 +224,7 @@ def test_tile_packed_stream_matches_dense(cuda, monkeypatch, cells):
     spec = pam.DictionarySpec(sigma=0.5 / cells[0])
     monkeypatch.setenv("PAM_TILE_TAU", "0")
     dense, rd = pam.fit_parallel(field, part, cfg, spec)
-    monkeypatch.setenv("PAM_TILE_TAU", str(2.0 ** -100))
+    monkeypatch.setenv("PAM_TILE_TAU", repr(tau))
     tiled, rt = pam.fit_parallel(field, part, cfg, spec)
     assert rt.device["cd_bytes"] < rd.device["cd_bytes"]  # tiles were actually dropped
     for a, b in zip(dense.locals, tiled.locals):

@@ -220,3 +220,40 @@ def test_config1_convergent_oracle_bit_exact(golden):
         np.testing.assert_array_equal(res["beta"], g[f"s{s}_beta"])
         assert res["iterations"] == int(g[f"s{s}_iterations"])
         assert bool(res["converged"]) == bool(g[f"s{s}_converged"])
+
+
+def test_tile_drop_threshold_is_below_parity(golden, monkeypatch):
+    """The CD stream drops 32-row tiles whose Shepard weights are all below
+    engine.DEFAULT_TILE_TAU (1e-16, the FP64 unit roundoff of a row of W,
+    which sums to 1).  Worst case of that: zero EVERY entry below tau (a
+    superset of the dropped tiles) in the oracle's full 3-round adaptive fit
+    of a C4 subdomain.  The dictionaries must stay identical and beta and the
+    round reports move by ~1e-13 relative, five orders below the 1e-8 parity
+    tolerance (measured 1e-13..8e-14 on C4 subdomains 0 and 1337)."""
+    from paper_2605_16564_b200.engine import DEFAULT_TILE_TAU
+
+    wl = workloads.config4(with_refined_eval=False)
+    g = golden("C4")
+    s = 2243
+    mesh = wl.field.mesh
+    boxes, _, _ = O.partition_boxes(mesh.counts, mesh.bounds, wl.shape)
+    b = boxes[s]
+    rows = O.subdomain_rows(mesh.centroids, b)
+    c = wl.config
+    cfg = dict(lam1=c.elastic.lam1, lam2=c.elastic.lam2, tol=c.elastic.tol, max_iters=c.elastic.max_iters,
+               k_top=c.k_top, m_max=c.m_max, eta=c.eta, m_q=c.m_q, max_rounds=c.max_rounds, offsets=c.offsets)
+    full = O.shepard_features
+
+    def dropped(p, cc, ww):
+        W = full(p, cc, ww)
+        W[W < DEFAULT_TILE_TAU] = 0.0
+        return W
+
+    monkeypatch.setattr(O, "shepard_features", dropped)
+    cen = mesh.centroids[rows]
+    od = O.fit_adaptive(cen, wl.field.values[rows], mesh.cell_size, b[0], b[1], cen,
+                        np.full(cen.shape[0], wl.spec.sigma), cfg)
+    np.testing.assert_array_equal(od["centers"], g[f"s{s}_centers"])
+    ref = g[f"s{s}_beta"]
+    assert np.abs(od["beta"] - ref).max() <= 1e-11 * np.abs(ref).max()
+    np.testing.assert_allclose(_rep_cols(od)[:, 2:], g[f"s{s}_reports"][:, [3, 4, 6]], rtol=1e-11)
