@@ -505,7 +505,8 @@ def run_c5(args):
         "evals": {"value": n_eval * args.steps / ev, "unit": "points/s"},
         "roofline": {"kernel": f"cd ({recs[0][3]} form)", "bound": "hbm", "achieved": streamed / cd / 1e9,
                      "peak": hbm, "unit": "GB/s", "frac": streamed / cd / 1e9 / hbm, "peak_source": src},
-        "kernel_seconds_per_step": {k: v / args.steps for k, v in recs[0][0].kernel_seconds.items()},
+        "kernel_seconds_per_step": {k: sum(r.kernel_seconds[k] for r, _, _, _ in recs) / args.steps
+                                    for k in recs[0][0].kernel_seconds},
         "clocks": clocks,
     }), flush=True)
     return 0

@@ -20,6 +20,9 @@ import numpy as np
 from .errors import NumericalError
 
 LIB_PATH = Path(__file__).resolve().parent / "libpam_b200.so"
+# A/B experiments only: PAM_LIB_PATH points at an alternative build of the same ABI
+if os.environ.get("PAM_LIB_PATH"):
+    LIB_PATH = Path(os.environ["PAM_LIB_PATH"])
 
 # status codes (pam_b200.h)
 PAM_OK = 0

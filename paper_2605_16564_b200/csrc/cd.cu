@@ -515,65 +515,6 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
 // and clearing stale tiles (by zero-page bulk copies or by shared stores) so
 // loads need no predicates was 12-14% slower than predicated packed loads.
 
-__device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
-  } while (!ok);
-}
-__device__ __forceinline__ bool mbar_test_s(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_expect_s(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_s(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-
-// 16-byte shared load at a 32-bit shared address; volatile keeps it behind
-// the mbarrier wait that published the data
-__device__ __forceinline__ void lds_v2(uint32_t addr, double& x, double& y) {
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(addr));
-}
-
-// bulk copy whose issue waits on `dep` (a register computed from the shared
-// loads of the destination slot): the async-proxy write cannot overtake them
-__device__ __forceinline__ void bulk_g2s_dep(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
-                                             double dep) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t"
-      "// dep %4" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar), "d"(dep)
-      : "memory");
-}
-
-__device__ __forceinline__ void cp_async16_dep(void* dst_smem, const void* src_gmem, double dep) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n\t// dep %2" ::"r"(smem_u32(dst_smem)),
-               "l"(src_gmem), "d"(dep)
-               : "memory");
-}
-
 // Run code of a tile mask made of at most two runs (tiles.cu run_cover):
 // a0 | la << 8 | b0 << 16 | lb << 24  (run A = tiles [a0, a0+la), B after it)
 __device__ __forceinline__ int tile_code(unsigned long long mk) {

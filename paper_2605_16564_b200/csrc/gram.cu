@@ -132,23 +132,44 @@ struct GramArgs {
 
 __device__ unsigned int g_gram_queue;
 
-// MT: max coordinates per lane (M <= 32*MT); SLOT: doubles per ring slot.
+// Lean covariance-form CD.  MT: coordinates per lane (M <= 32*MT, MT even);
+// SLOT: doubles per ring slot (cps = SLOT / ldg columns per slot).
+//
+// Paired layout: lane l owns coordinates 64u + 2l + {0,1} in c[2u], c[2u+1],
+// so each AXPY element pair is one 16-byte shared load.  The coordinate loop
+// is NOT unrolled over chunks (an unrolled loop over MT chunks overflowed the
+// instruction cache at M = 512, 0.57 of HBM): the current 64-coordinate
+// chunk's two values live in (cur0, cur1), selected once per chunk and
+// updated alongside c, so c_j is one shuffle away.  Per-chunk parameters
+// (beta, col_sq, 1/(col_sq+lam2)) are prefetched one chunk ahead into a
+// per-warp shared block; the division is the reciprocal plus one FMA
+// correction, as in cd.cu's lean kernel.
 template <int MT, int STAGES, int WPC, int SLOT>
 __global__ void __launch_bounds__(WPC * 32, 1) cd_gram_kernel(const GramArgs a) {
+  static_assert(MT % 2 == 0, "paired layout");
+  constexpr int MP = MT / 2;  // 16-byte pairs per lane
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  double* ring = reinterpret_cast<double*>(smem_raw) + static_cast<size_t>(warp) * STAGES * SLOT;
-  uint64_t* bars =
-      reinterpret_cast<uint64_t*>(reinterpret_cast<double*>(smem_raw) + WPC * STAGES * SLOT) +
-      warp * STAGES;
+  double* const ring = reinterpret_cast<double*>(smem_raw) + static_cast<size_t>(warp) * STAGES * SLOT;
+  uint64_t* const bars =
+      reinterpret_cast<uint64_t*>(reinterpret_cast<double*>(smem_raw) + WPC * STAGES * SLOT) + warp * STAGES;
+  double* const pblk = reinterpret_cast<double*>(
+                           reinterpret_cast<uint64_t*>(reinterpret_cast<double*>(smem_raw) + WPC * STAGES * SLOT) +
+                           WPC * STAGES) +
+                       warp * 192;
+  double* const pb = pblk;          // [64] beta of the chunk
+  double* const pc = pblk + 64;     // [64] col_sq
+  double* const pinv = pblk + 128;  // [64] 1 / (col_sq + lam2)
   if (lane == 0) {
-    for (int st = 0; st < STAGES; ++st) mbar_init(&bars[st], 1);
+    for (int i = 0; i < STAGES; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
-    fence_proxy_async_smem();
   }
   __syncwarp();
-  uint32_t g_issue = 0, g_cons = 0;
+  const uint32_t ring_s = smem_u32(ring);
+  const uint32_t bar_s = smem_u32(bars);
+  int ist = 0, cst = 0;  // issue / consume ring slots
+  uint32_t ph = 0;       // consume phase parity
   const unsigned total_warps = gridDim.x * WPC;
   unsigned item = warp * gridDim.x + blockIdx.x;
 
@@ -159,107 +180,165 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_gram_kernel(const GramArgs a) 
       const int64_t doff = a.dict_off[s];
       const double* Gs = a.G + a.g_off[s];
       const int ldgs = a.ldg[s];
-      const int cps = max(1, SLOT / ldgs);          // columns per ring slot
-      const int groups = (M + cps - 1) / cps;       // slots per pass over G
+      const int cps = max(1, SLOT / ldgs);     // columns per ring slot
+      const int groups = (M + cps - 1) / cps;  // slots per pass over G
       const double lam1 = a.lam1[s], lam2 = a.lam2[s], tol = a.tol[s];
       const int max_iters = a.max_iters[s];
+      double* betas = a.beta + doff;
 
       double c[MT];
 #pragma unroll
-      for (int t = 0; t < MT; ++t) {
-        const int k = 32 * t + lane;
-        c[t] = (k < M) ? a.q[doff + k] : 0.0;
+      for (int u = 0; u < MP; ++u) {
+        const int k = 64 * u + 2 * lane;
+        c[2 * u] = (k < M) ? a.q[doff + k] : 0.0;
+        c[2 * u + 1] = (k + 1 < M) ? a.q[doff + k + 1] : 0.0;
       }
-      const int64_t total = (int64_t)(max_iters + 1) * groups;  // prologue pass + sweeps
-      int64_t issued = 0;
-      int next_group = 0;
-      auto issue_one = [&]() {
+      // issue side: group stream = [prologue] + max_iters passes (32-bit: host envelope)
+      const int total = (max_iters + 1) * groups;
+      int issued = 0, next_group = 0;
+      auto issue_one = [&](double dep) {
         if (lane == 0) {
-          const int st = g_issue % STAGES;
           const int c0 = next_group * cps;
           const int nc = min(cps, M - c0);
           const uint32_t nb = static_cast<uint32_t>(nc) * ldgs * sizeof(double);
-          fence_proxy_async_smem();
-          mbar_arrive_expect_tx(&bars[st], nb);
-          tma_load_1d(ring + st * SLOT, Gs + (int64_t)c0 * ldgs, nb, &bars[st]);
+          const uint32_t bar = bar_s + ist * 8;
+          mbar_expect_s(bar, nb);
+          bulk_g2s_dep(ring_s + ist * (SLOT * 8), Gs + (int64_t)c0 * ldgs, nb, bar, dep);
         }
-        ++g_issue;
+        if (++ist == STAGES) ist = 0;
         ++issued;
         if (++next_group == groups) next_group = 0;
       };
-      for (int q0 = 0; q0 < STAGES && issued < total; ++q0) issue_one();
-      int64_t consumed = 0;
-      const double* slot = nullptr;
-      auto column = [&](int j) -> const double* {
-        const int in = j % cps;
-        if (in == 0) {
-          const int st = g_cons % STAGES;
-          mbar_wait(&bars[st], (g_cons / STAGES) & 1u);
-          ++g_cons;
-          ++consumed;
-          slot = ring + st * SLOT;
+      for (int q0 = 0; q0 < STAGES && issued < total; ++q0) issue_one(0.0);
+      int consumed = 0;
+      int in_slot = cps;  // columns left in the current slot (cps -> acquire next)
+      uint32_t col_s = 0;
+      // shared address of column j (columns arrive in order; slot acquired on demand)
+      auto column = [&]() -> uint32_t {
+        if (in_slot == cps) {
+          mbar_wait_s(bar_s + cst * 8, ph);
+          col_s = ring_s + cst * (SLOT * 8);
+          in_slot = 0;
+        } else {
+          col_s += ldgs * 8;
         }
-        return slot + in * ldgs;
+        ++in_slot;
+        return col_s;
       };
-      auto release = [&](int j) {  // after the last column of a slot
-        if ((j % cps) == cps - 1 || j == M - 1) {
-          __syncwarp();
-          if (issued < total) issue_one();
+      // after the last use of a column: free its slot when it was the slot's last
+      auto release = [&](bool last_col_of_pass, double dep) {
+        if (in_slot == cps || last_col_of_pass) {
+          in_slot = cps;
+          if (++cst == STAGES) {
+            cst = 0;
+            ph ^= 1u;
+          }
+          ++consumed;
+          if (issued < total) issue_one(dep);
         }
+      };
+      auto axpy = [&](uint32_t col, double d) {
+        double dep = 0.0;
+#pragma unroll
+        for (int u = 0; u < MP; ++u) {
+          double g0, g1;
+          lds_v2(col + 16u * lane + 512u * u, g0, g1);
+          c[2 * u] = fma(-d, g0, c[2 * u]);
+          c[2 * u + 1] = fma(-d, g1, c[2 * u + 1]);
+          dep += g0;
+        }
+        return dep;
       };
 
       // prologue: c = q - G beta0 (warm start, adaptive.py:268)
       for (int j = 0; j < M; ++j) {
-        const double* col = column(j);
-        const double b0 = a.beta[doff + j];
-        if (b0 != 0.0) {
-#pragma unroll
-          for (int t = 0; t < MT; ++t)
-            if (32 * t + lane < M) c[t] = __dsub_rn(c[t], __dmul_rn(b0, col[32 * t + lane]));
+        const uint32_t col = column();
+        const double b0 = betas[j];
+        double dep = 0.0;
+        if (b0 != 0.0) dep = axpy(col, b0);
+        else {
+          double g0, g1;
+          lds_v2(col + 16u * lane, g0, g1);  // the slot is read before it is refilled
+          dep = g0;
         }
-        release(j);
+        release(j == M - 1, dep);
       }
 
+      const int nchunk = (M + 63) / 64;
+      double nb0 = 0.0, nb1 = 0.0, nc0 = 0.0, nc1 = 0.0;
+      auto fetch = [&](int q) {
+        const int k0 = 64 * q + lane, k1 = k0 + 32;
+        nb0 = (k0 < M) ? betas[k0] : 0.0;
+        nb1 = (k1 < M) ? betas[k1] : 0.0;
+        nc0 = (k0 < M) ? a.col_sq[doff + k0] : 0.0;
+        nc1 = (k1 < M) ? a.col_sq[doff + k1] : 0.0;
+      };
+      fetch(0);
       int sweeps_done = 0, conv = 0;
       for (int sw = 0; sw < max_iters; ++sw) {
         double max_delta = 0.0, acc_max = 0.0;
+        for (int q = 0; q < nchunk; ++q) {
+          const int nc = min(64, M - 64 * q);
+          __syncwarp();
+          // one chunk: the block keeps the updated betas across sweeps (a
+          // prefetch would read them before this sweep's write-back)
+          if (sw == 0 || nchunk > 1) {
+            pb[lane] = nb0;
+            pb[32 + lane] = nb1;
+            pc[lane] = nc0;
+            pc[32 + lane] = nc1;
+            const double d0 = __dadd_rn(nc0, lam2), d1 = __dadd_rn(nc1, lam2);
+            pinv[lane] = d0 > 0.0 ? __ddiv_rn(1.0, d0) : 0.0;
+            pinv[32 + lane] = d1 > 0.0 ? __ddiv_rn(1.0, d1) : 0.0;
+            if (nchunk > 1) fetch(q + 1 < nchunk ? q + 1 : 0);
+          }
+          __syncwarp();
+          // this chunk's pair of c values (runtime q -> static selects, once per chunk)
+          double cur0 = 0.0, cur1 = 0.0;
 #pragma unroll
-        for (int t = 0; t < MT; ++t) {
-          if (32 * t < M) {
-            const int nc = min(32, M - 32 * t);
-            double bl = 0.0, csl = 0.0;
-            if (lane < nc) {
-              bl = a.beta[doff + 32 * t + lane];
-              csl = a.col_sq[doff + 32 * t + lane];
+          for (int u = 0; u < MP; ++u) {
+            if (u == q) {
+              cur0 = c[2 * u];
+              cur1 = c[2 * u + 1];
             }
-            for (int jj = 0; jj < nc; ++jj) {
-              const int j = 32 * t + jj;
-              const double* col = column(j);
-              const double cj = __shfl_sync(0xffffffffu, c[t], jj);
-              const double b_old = __shfl_sync(0xffffffffu, bl, jj);
-              const double cs = __shfl_sync(0xffffffffu, csl, jj);
-              const double dn = __dadd_rn(cs, lam2);
-              const double z = __dadd_rn(__dmul_rn(cs, b_old), cj);
-              double b_new = 0.0;
-              if (dn > 0.0) {
-                double mag = __dsub_rn(fabs(z), lam1);
-                if (mag < 0.0) mag = 0.0;
-                b_new = __ddiv_rn(z >= 0.0 ? mag : -mag, dn);
-              }
-              if (b_new != b_old) {
-                const double d = __dsub_rn(b_new, b_old);
-#pragma unroll
-                for (int t2 = 0; t2 < MT; ++t2)
-                  if (32 * t2 + lane < M) c[t2] = __dsub_rn(c[t2], __dmul_rn(d, col[32 * t2 + lane]));
-                if (lane == jj) bl = b_new;
-                max_delta = fmax(max_delta, fabs(d));
-              }
-              release(j);
+          }
+          for (int r = 0; r < nc; ++r) {
+            const int j = 64 * q + r;
+            const uint32_t col = column();
+            const double cj = __shfl_sync(0xffffffffu, (r & 1) ? cur1 : cur0, r >> 1);
+            const double b_old = pb[r];
+            const double cs = pc[r];
+            const double inv = pinv[r];
+            const double dn = __dadd_rn(cs, lam2);
+            const double z = __dadd_rn(__dmul_rn(cs, b_old), cj);
+            const double np_ = __dsub_rn(z, lam1), nn_ = __dadd_rn(z, lam1);
+            const double qp = __dmul_rn(np_, inv), qn = __dmul_rn(nn_, inv);
+            const double bp = fma(fma(-qp, dn, np_), inv, qp);
+            const double bn = fma(fma(-qn, dn, nn_), inv, qn);
+            const double b_new = np_ > 0.0 ? bp : (nn_ < 0.0 ? bn : 0.0);
+            const double d = __dsub_rn(b_new, b_old);
+            double dep;
+            {
+              double g0, g1;
+              lds_v2(col + 16u * lane + 512u * q, g0, g1);
+              cur0 = fma(-d, g0, cur0);
+              cur1 = fma(-d, g1, cur1);
+              dep = axpy(col, d) + g0;
             }
-            if (lane < nc) {
-              a.beta[doff + 32 * t + lane] = bl;
-              acc_max = fmax(acc_max, fabs(bl));
-            }
+            if (lane == 0) pb[r] = b_new;
+            const double ad = fabs(d);
+            max_delta = ad > max_delta ? ad : max_delta;
+            release(j == M - 1, dep);
+          }
+          __syncwarp();
+          const int k0 = 64 * q + lane, k1 = k0 + 32;
+          if (k0 < M) {
+            betas[k0] = pb[lane];
+            acc_max = fmax(acc_max, fabs(pb[lane]));
+          }
+          if (k1 < M) {
+            betas[k1] = pb[32 + lane];
+            acc_max = fmax(acc_max, fabs(pb[32 + lane]));
           }
         }
         const double mabs = warp_max(acc_max);
@@ -269,10 +348,12 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_gram_kernel(const GramArgs a) 
           break;
         }
       }
-      while (consumed < issued) {  // drain speculative prefetches
-        const int st = g_cons % STAGES;
-        mbar_wait(&bars[st], (g_cons / STAGES) & 1u);
-        ++g_cons;
+      while (consumed < issued) {  // drain the prefetched groups of the pass that will not run
+        mbar_wait_s(bar_s + cst * 8, ph);
+        if (++cst == STAGES) {
+          cst = 0;
+          ph ^= 1u;
+        }
         ++consumed;
       }
       __syncwarp();
@@ -289,7 +370,8 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_gram_kernel(const GramArgs a) 
 
 template <int MT, int STAGES, int WPC, int SLOT>
 int launch_gram_cd(const GramArgs& a, cudaStream_t stream) {
-  const size_t smem = static_cast<size_t>(WPC) * STAGES * (SLOT * sizeof(double) + sizeof(uint64_t));
+  const size_t smem = static_cast<size_t>(WPC) * STAGES * (SLOT * sizeof(double) + sizeof(uint64_t)) +
+                      static_cast<size_t>(WPC) * 192 * sizeof(double);
   static bool configured = false;
   if (!configured) {
     PAM_CUDA_CHECK(cudaFuncSetAttribute(cd_gram_kernel<MT, STAGES, WPC, SLOT>,

@@ -155,6 +155,66 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// 32-bit shared-address variants used by the lean streaming kernels (cd.cu, gram.cu)
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ bool mbar_test_s(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_expect_s(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_s(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+// 16-byte shared load at a 32-bit shared address; volatile keeps it behind
+// the mbarrier wait that published the data
+__device__ __forceinline__ void lds_v2(uint32_t addr, double& x, double& y) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(addr));
+}
+
+// bulk copy whose issue waits on `dep` (a register computed from the shared
+// loads of the destination slot): the async-proxy write cannot overtake them
+__device__ __forceinline__ void bulk_g2s_dep(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                             double dep) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t"
+      "// dep %4" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "d"(dep)
+      : "memory");
+}
+
+__device__ __forceinline__ void cp_async16_dep(void* dst_smem, const void* src_gmem, double dep) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n\t// dep %2" ::"r"(smem_u32(dst_smem)),
+               "l"(src_gmem), "d"(dep)
+               : "memory");
+}
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Kept-tile runs per column of the tile-packed design matrices (tiles.cu):
