@@ -127,7 +127,7 @@ __global__ void scatter_kernel(int64_t P, const int64_t* __restrict__ owner,
 //   exactly rounded by one DFMA, 2^(f/2048) by a degree-3 polynomial
 //   (truncation <= 3.4e-17 relative), 2^(n/2048) = 2^(n>>11) * T[n & 2047]
 //   with T in shared memory and 2^(n>>11) added into T's exponent field by an
-//   integer add (no FP64 op).  Terms below 2^-1022 are flushed to 0; a point
+//   integer add (no FP64 op).  Terms below 2^-1022 are exactly 0; a point
 //   whose every term underflows (den < 1e-280, ~27 widths from all entries) is
 //   redone with the reference's exact max-shifted two-pass form.
 // Per-term relative error ~1e-16*(1+|L|), the same order as the reference's
@@ -160,12 +160,11 @@ __device__ __forceinline__ double exp_neg_scaled(double d2, double g, const unsi
   const unsigned lo = static_cast<unsigned>(sb);
   const unsigned long long tw = tab[lo & (XT - 1)];
   const unsigned hi = static_cast<unsigned>(tw >> 32) + (lo << 9);
-  // below 2^-1022 only the high word is cleared: the term becomes a denormal
-  // < 2^-1022 (relative effect < 1e-25 on any denominator >= 1e-280)
-  const double Ts = __hiloint2double(static_cast<int>((sb >= EXP_SHIFT_BITS + EXP_NMIN) ? hi : 0u),
-                                     static_cast<int>(static_cast<unsigned>(tw)));
+  const double Ts = __hiloint2double(static_cast<int>(hi), static_cast<int>(static_cast<unsigned>(tw)));
   const double p = fma(f, fma(f, fma(f, EXP_C3, EXP_C2), EXP_C1), 1.0);
-  return Ts * p;
+  // terms below 2^-1022 (and |t| beyond the shift trick's range, where f and
+  // the scale are meaningless) are exactly 0: a select, not an FP64 op
+  return (sb >= EXP_SHIFT_BITS + EXP_NMIN) ? Ts * p : 0.0;
 }
 
 // Variant R (PAM_EVAL_TAB=256): a 256-entry table replicated 16 times so a
@@ -191,10 +190,9 @@ __device__ __forceinline__ double exp_neg_scaled_r(double d2, double g, const un
   const unsigned lo = static_cast<unsigned>(sb);
   const unsigned long long tw = tab[((lo & (XR - 1)) * XR_REP) + rep];
   const unsigned hi = static_cast<unsigned>(tw >> 32) + (lo << (20 - XR_BITS));
-  const double Ts = __hiloint2double(static_cast<int>((sb >= EXP_SHIFT_BITS + EXR_NMIN) ? hi : 0u),
-                                     static_cast<int>(static_cast<unsigned>(tw)));
+  const double Ts = __hiloint2double(static_cast<int>(hi), static_cast<int>(static_cast<unsigned>(tw)));
   const double p = fma(f, fma(f, fma(f, fma(f, EXR_C4, EXR_C3), EXR_C2), EXR_C1), 1.0);
-  return Ts * p;
+  return (sb >= EXP_SHIFT_BITS + EXR_NMIN) ? Ts * p : 0.0;
 }
 
 // the reference's exact max-shifted two-pass Shepard sum (rbf.py:152-167) for

@@ -222,3 +222,22 @@ def test_global_eval_underflow_rows_fall_back_exactly(cuda):
     ref, _ = O.global_evaluate(pts, [(b.lo, b.hi, b.open_hi) for b in part.boxes], olocs)
     assert np.isfinite(ref).all()
     np.testing.assert_allclose(sur.evaluate(pts), ref, rtol=1e-10)
+
+
+def test_local_eval_far_points_use_exact_fallback(cuda):
+    """LocalSurrogate.evaluate at points 1e3..1e9 widths from every entry: the
+    table exp returns exact zeros there (also beyond the range of its rounding
+    shift), so the rows go through the max-shifted two-pass form like the
+    reference (rbf.py:152-167) instead of producing garbage."""
+    rng = np.random.default_rng(5)
+    c = rng.random((20, 3))
+    w = np.full(20, 0.01)
+    beta = rng.standard_normal(20)
+    loc = pam.LocalSurrogate(dictionary=pam.RbfDictionary(centers=c, widths=w), beta=beta)
+    dirs = rng.standard_normal((60, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    dist = np.repeat(10.0 ** np.arange(1, 7.5, 0.5), 5)[:60]  # 10 .. 3e7 (1e3 .. 3e9 widths)
+    pts = 0.5 + dirs * dist[:, None]
+    ref = O.surrogate_eval(pts, c, w, beta)
+    assert np.isfinite(ref).all()
+    np.testing.assert_allclose(loc.evaluate(pts), ref, rtol=1e-12)
