@@ -333,15 +333,18 @@ def test_centroid_values_within_max_residual(cuda):
     assert np.max((vals - field.values) ** 2 * field.mesh.cell_measure) <= worst * (1 + 1e-9)
 
 
-def test_subdomain_batch_api_c5_sample(cuda):
-    """C5 shape (unit boxes, 1000 random samples, jittered lattice) on a 32-box sample."""
-    p = workloads.config5(M=64, n_sub=32, n_eval=0)
+@pytest.mark.parametrize("M", [64, 128, 256, 512])
+def test_subdomain_batch_api_c5_sample(cuda, M):
+    """C5 shape (unit boxes, 1000 random samples, jittered lattice) on a 32-box sample,
+    every centre count of the sweep (the covariance-form CD runs a different
+    register configuration for each)."""
+    p = workloads.config5(M=M, n_sub=32, n_eval=0)
     res = pam.fit_subdomains(p)
     c = p.config
-    for s in (0, 17, 31):
+    for s in ((0, 17, 31) if M <= 128 else (0, 31)):
         a, b = p.row_off[s], p.row_off[s + 1]
-        cen = p.centres[s * 64:(s + 1) * 64]
-        W = O.shepard_features(p.points[a:b], cen, p.widths[s * 64:(s + 1) * 64])
+        cen = p.centres[s * M:(s + 1) * M]
+        W = O.shepard_features(p.points[a:b], cen, p.widths[s * M:(s + 1) * M])
         o = O.fit_log(p.values[a:b], W, c.elastic.lam1, c.elastic.lam2, c.elastic.tol, c.elastic.max_iters)
         assert np.max(np.abs(res.beta[s] - o["beta"])) <= BETA_TOL * max(1, np.abs(o["beta"]).max())
         assert res.rounds[0].sweeps[s] == o["iterations"] or abs(res.rounds[0].sweeps[s] - o["iterations"]) <= 1
