@@ -377,14 +377,18 @@ def run_ours(args):
                      "dense_equivalent_bytes_per_launch": cd_dense / max(cd_launches, 1),
                      "tile_tau": __import__("paper_2605_16564_b200.engine", fromlist=["x"]).tile_tau(),
                      "step_share": cd_s / elapsed if elapsed else None},
-        "eval_roofline": {"kernel": "eval_kernel (locate + owner sort + two-pass Shepard + exp)",
+        "eval_roofline": {"kernel": "eval_kernel (locate + owner sort + one-pass Shepard sum, table-driven FP64 exp)",
                           "bound": "fp64", "unit": "GFLOP/s",
                           "flops_per_pair": 3 * 3 + 4 + 20,
                           "flop_convention": "SURVEY 8d: M_owner*(3d+4+E) per point, E=20 FP64 ops per exp",
                           "pairs_per_step": eval_pairs,
                           "achieved": eval_pairs * 33 / (eval_s / args.steps) / 1e9,
                           "peak": fp64_peak / 1e9, "peak_source": "measured (pam_probe_fp64, FMA=2)",
-                          "frac": eval_pairs * 33 / (eval_s / args.steps) / fp64_peak},
+                          "frac": eval_pairs * 33 / (eval_s / args.steps) / fp64_peak,
+                          # issued FP64 instructions (SASS: 15 per pair) against the pipe's
+                          # instruction rate (peak flop/s / 2): the honest pipe utilisation
+                          "fp64_instr_per_pair": 15,
+                          "issued_pipe_frac": eval_pairs * 15 / (eval_s / args.steps) / (fp64_peak / 2)},
         "kernel_seconds_per_step": {k: v / args.steps for k, v in kt.items()},
         "cd_rounds": [{**d, "achieved_gbs": d["bytes"] / d["seconds"] / 1e9 if d["seconds"] else None,
                        "max_over_mean_fit": d["max_fit_bytes"] / d["mean_fit_bytes"] if d["mean_fit_bytes"] else None}
