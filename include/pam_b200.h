@@ -32,6 +32,13 @@
  *                   the packed W buffer; column-major with leading dimension
  *                   ld[s] (int32, multiple of 16): W_s[i, j] = W[w_off+j*ld+i].
  *
+ * Concurrency: the batched CD kernels (pam_cd_*_f64) balance subdomains
+ * with a per-library device work counter, so CD calls must not run
+ * concurrently on two streams of one device (the reference's own threading
+ * model is one fit loop per process, partition.py:185-198).  The evaluation
+ * entry points keep no global state (pam_eval_f64's tile queue lives in the
+ * caller's workspace) and may overlap.
+ *
  * Citations are relative to the reference package root pkg/src/fieldfit/.
  */
 #ifndef PAM_B200_H

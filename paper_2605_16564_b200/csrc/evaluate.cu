@@ -149,7 +149,6 @@ constexpr long long EXP_NMIN = -1022LL * XT;        // 2^(n/2048) >= 2^-1022
 // n = 2048 (n >> 11) + j: one integer multiply-add applies the 2^(n >> 11)
 // scale (see ensure_exp2_table)
 __device__ unsigned long long g_exp2_table[XT];
-__device__ unsigned long long g_eval_queue;
 
 // exp(-g * d2) with g = K/(2 w^2) -- see the block comment above
 __device__ __forceinline__ double exp_neg_scaled(double d2, double g, const unsigned long long* tab) {
@@ -230,7 +229,7 @@ eval_kernel(int64_t P, const double* __restrict__ pts, const int64_t* __restrict
             const int32_t* __restrict__ m_cur, const double* __restrict__ centres,
             const double* __restrict__ widths, const double* __restrict__ beta,
             const int32_t* __restrict__ log_flag, int single_m, int single_exp,
-            double* __restrict__ out, int64_t* err) {
+            double* __restrict__ out, int64_t* err, unsigned long long* queue) {
   constexpr int REC = (D + 2 + 1) & ~1;  // staged record: centre, g, beta (16-byte aligned)
   constexpr int TAB = REPL ? XR * XR_REP : XT;
   __shared__ unsigned long long tab[TAB];
@@ -243,12 +242,17 @@ eval_kernel(int64_t P, const double* __restrict__ pts, const int64_t* __restrict
   const int rep = lane & (XR_REP - 1);
   double* const st = stage[warp];
   const int64_t n_tiles = (P + 32 * PT - 1) / (32 * PT);
-  // persistent warps pulling 32*PT-point tiles from a global queue: balanced
-  // whatever the owner-run mix of a tile and however many CTAs are resident
+  // persistent warps pulling 32*PT-point tiles from a queue counter in the
+  // caller's workspace (balanced whatever the owner-run mix of a tile and
+  // however many CTAs are resident; no global state, so concurrent calls on
+  // different streams are independent); queue == nullptr: one tile per warp
+  int64_t tile = static_cast<int64_t>(blockIdx.x) * EVAL_WARPS + warp;
   while (true) {
-    unsigned long long tq = 0;
-    if (lane == 0) tq = atomicAdd(&g_eval_queue, 1ull);
-    const int64_t tile = static_cast<int64_t>(__shfl_sync(0xffffffffu, tq, 0));
+    if (queue) {
+      unsigned long long tq = 0;
+      if (lane == 0) tq = atomicAdd(queue, 1ull);
+      tile = static_cast<int64_t>(__shfl_sync(0xffffffffu, tq, 0));
+    }
     if (tile >= n_tiles) break;
     const int64_t base = tile * (32 * PT);
     bool have[PT];
@@ -337,6 +341,7 @@ eval_kernel(int64_t P, const double* __restrict__ pts, const int64_t* __restrict
       if (nxt == INT64_MAX) break;
       cur = nxt;
     }
+    if (!queue) break;
   }
 }
 
@@ -384,7 +389,8 @@ template <int D, int PT, bool REPL>
 int launch_eval_v(cudaStream_t st, int64_t P, const double* pts, const int64_t* perm,
                   const int64_t* sorted_owner, const int64_t* dict_off, const int32_t* m_cur,
                   const double* centres, const double* widths, const double* beta,
-                  const int32_t* log_flag, int single_m, int single_exp, double* out, int64_t* err) {
+                  const int32_t* log_flag, int single_m, int single_exp, double* out, int64_t* err,
+                  unsigned long long* queue) {
   static int grid_cap = 0;
   if (grid_cap == 0) {
     int dev = 0, sms = 148, per_sm = 1;
@@ -398,13 +404,14 @@ int launch_eval_v(cudaStream_t st, int64_t P, const double* pts, const int64_t* 
                                                                  EVAL_WARPS * 32, 0));
     grid_cap = sms * std::max(per_sm, 1);
   }
-  const int64_t ctas = std::min<int64_t>(grid_cap, ceil_div(P, static_cast<int64_t>(EVAL_WARPS) * 32 * PT));
-  void* qaddr = nullptr;
-  PAM_CUDA_CHECK(cudaGetSymbolAddress(&qaddr, g_eval_queue));
-  PAM_CUDA_CHECK(cudaMemsetAsync(qaddr, 0, sizeof(unsigned long long), st));
+  // with a queue: a persistent grid of one wave; without: one tile per warp
+  const int64_t tiles_ctas = ceil_div(P, static_cast<int64_t>(EVAL_WARPS) * 32 * PT);
+  const int64_t ctas = queue ? std::min<int64_t>(grid_cap, tiles_ctas) : tiles_ctas;
+  if (ctas > 0x7fffffffLL) return PAM_ERR_ARG;
+  if (queue) PAM_CUDA_CHECK(cudaMemsetAsync(queue, 0, sizeof(unsigned long long), st));
   eval_kernel<D, PT, REPL><<<(unsigned)ctas, EVAL_WARPS * 32, 0, st>>>(
       P, pts, perm, sorted_owner, dict_off, m_cur, centres, widths, beta, log_flag, single_m,
-      single_exp, out, err);
+      single_exp, out, err, queue);
   PAM_LAUNCH_CHECK("eval_kernel");
   return PAM_OK;
 }
@@ -413,11 +420,12 @@ template <int D>
 int launch_eval(cudaStream_t st, int64_t P, const double* pts, const int64_t* perm,
                 const int64_t* sorted_owner, const int64_t* dict_off, const int32_t* m_cur,
                 const double* centres, const double* widths, const double* beta,
-                const int32_t* log_flag, int single_m, int single_exp, double* out, int64_t* err) {
+                const int32_t* log_flag, int single_m, int single_exp, double* out, int64_t* err,
+                unsigned long long* queue) {
   const int rc = ensure_exp2_table();
   if (rc != PAM_OK) return rc;
 #define PAM_EVAL_ARGS st, P, pts, perm, sorted_owner, dict_off, m_cur, centres, widths, beta, log_flag, \
-                      single_m, single_exp, out, err
+                      single_m, single_exp, out, err, queue
   if (eval_pt() == 4) {
     if (eval_repl()) return launch_eval_v<D, 4, true>(PAM_EVAL_ARGS);
     return launch_eval_v<D, 4, false>(PAM_EVAL_ARGS);
@@ -436,7 +444,8 @@ int grid_for(int64_t n, int threads) {
 using namespace pam;
 
 extern "C" int64_t pam_eval_workspace_bytes(int64_t P, int64_t S) {
-  // owner, perm, sorted_owner (P each) + counts, cursor (S) + start (S+1)
+  // owner, perm, sorted_owner (P each) + counts, cursor (S) + start (S+1);
+  // the slack holds the evaluation kernel's tile-queue counter
   return 3 * P * 8 + (3 * S + 1) * 8 + 256;
 }
 
@@ -468,6 +477,7 @@ extern "C" int pam_eval_f64(int dim, int64_t P, const double* pts, const int32_t
   unsigned long long* counts = reinterpret_cast<unsigned long long*>(sorted_owner + P);
   unsigned long long* cursor = counts + S;
   unsigned long long* start = cursor + S;
+  unsigned long long* queue = start + S + 1;  // in the workspace slack
   int rc = pam_locate_f64(dim, P, pts, shape, edges, owner, err, stream);
   if (rc != PAM_OK) return rc;
   PAM_CUDA_CHECK(cudaMemsetAsync(counts, 0, S * sizeof(unsigned long long), st));
@@ -484,12 +494,12 @@ extern "C" int pam_eval_f64(int dim, int64_t P, const double* pts, const int32_t
   PAM_LAUNCH_CHECK("scatter_kernel");
   if (dim == 1)
     return launch_eval<1>(st, P, pts, perm, sorted_owner, dict_off, m_cur, centres, widths, beta,
-                          log_flag, 0, 0, out, err);
+                          log_flag, 0, 0, out, err, queue);
   if (dim == 2)
     return launch_eval<2>(st, P, pts, perm, sorted_owner, dict_off, m_cur, centres, widths, beta,
-                          log_flag, 0, 0, out, err);
+                          log_flag, 0, 0, out, err, queue);
   return launch_eval<3>(st, P, pts, perm, sorted_owner, dict_off, m_cur, centres, widths, beta,
-                        log_flag, 0, 0, out, err);
+                        log_flag, 0, 0, out, err, queue);
 }
 
 extern "C" int pam_shepard_eval_f64(int dim, int64_t P, const double* pts, int64_t M,
@@ -502,10 +512,10 @@ extern "C" int pam_shepard_eval_f64(int dim, int64_t P, const double* pts, int64
   const int m = static_cast<int>(M);
   if (dim == 1)
     return launch_eval<1>(st, P, pts, nullptr, nullptr, nullptr, nullptr, centres, widths, beta,
-                          nullptr, m, exp_out, out, err);
+                          nullptr, m, exp_out, out, err, nullptr);
   if (dim == 2)
     return launch_eval<2>(st, P, pts, nullptr, nullptr, nullptr, nullptr, centres, widths, beta,
-                          nullptr, m, exp_out, out, err);
+                          nullptr, m, exp_out, out, err, nullptr);
   return launch_eval<3>(st, P, pts, nullptr, nullptr, nullptr, nullptr, centres, widths, beta,
-                        nullptr, m, exp_out, out, err);
+                        nullptr, m, exp_out, out, err, nullptr);
 }
