@@ -896,6 +896,308 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
   }
 }
 
+// ----------------------------------------------------------------------------
+// Column-pair tile CD for batches of few fits (<= a few per SM: BASELINE
+// configs 2-3, 64-256 fits of 1,024 rows).  With one or two fits per SM a
+// fit's per-column dependency chain (dot -> 5-level reduction -> soft
+// threshold -> AXPY, ~0.55 us) is the whole cost, and registers/shared memory
+// are plentiful.  So columns are taken in pairs (j, j+1): both dots against the
+// same residual r_{j-1}, both warp reductions interleaved, then the soft
+// thresholds in order with column j+1's dot corrected by the Gram entry,
+//   W_{j+1} . r_j = W_{j+1} . r_{j-1} - d_j (W_j . W_{j+1}),
+// exact in exact arithmetic (only the rounding of the length-N dot products
+// differs from the reference's sequential sums, as for every CD form here;
+// SURVEY F2), then both updates.  The pair products g_j = W_j . W_{j+1} (j even)
+// are formed in the prologue pass from the same staged tiles.  The ring and
+// copy issue are the lean kernel's; a fit's run codes and packed offsets are
+// staged in shared memory once per launch.
+template <int R, int STAGES, int WPC>
+__global__ void __launch_bounds__(WPC * 32, 1) cd_pipe_kernel(const CdArgs a, int gcap) {
+  constexpr int SLOT = R * 32;
+  static_assert(R % 2 == 0 && R <= 32, "paired-row layout");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  // per warp: ring[STAGES][SLOT] | pb/pc/pinv[32] | g[gcap] | codes[gcap] | offs[gcap]
+  const size_t per_warp = static_cast<size_t>(STAGES) * SLOT * 8 + 96 * 8 + static_cast<size_t>(gcap) * 16;
+  unsigned char* const wbase = smem_raw + static_cast<size_t>(warp) * per_warp;
+  double* const ring = reinterpret_cast<double*>(wbase);
+  double* const pb = ring + STAGES * SLOT;
+  double* const pc = pb + 32;
+  double* const pinv = pb + 64;
+  double* const gn = pb + 96;
+  int* const codes = reinterpret_cast<int*>(gn + gcap);
+  int* const offs = codes + gcap;
+  uint64_t* const bars_all = reinterpret_cast<uint64_t*>(smem_raw + WPC * per_warp);
+  uint64_t* const bars = bars_all + warp * STAGES;
+  // zero block 16-byte aligned after the barriers (16-byte shared loads)
+  double* const zero_blk = reinterpret_cast<double*>(bars_all + ((WPC * STAGES + 1) & ~1));
+  const uint32_t ring_s = smem_u32(ring);
+  const uint32_t bar_s = smem_u32(bars);
+  const uint32_t zero_s = smem_u32(zero_blk) + 16u * lane;
+  const int half = lane >> 4;
+
+  for (int i = threadIdx.x; i < SLOT; i += WPC * 32) zero_blk[i] = 0.0;
+  if (lane == 0) {
+    for (int i = 0; i < STAGES; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  int st = 0, ist = 0;
+  uint32_t ph = 0;
+  unsigned item = warp * gridDim.x + blockIdx.x;
+  const unsigned total_warps = gridDim.x * WPC;
+
+  while (item < a.S) {
+    const int64_t s = a.order ? a.order[item] : static_cast<int64_t>(item);
+    if (a.active == nullptr || a.active[s] != 0) {
+      const int64_t r0 = a.row_off[s];
+      const int N = static_cast<int>(a.row_off[s + 1] - r0);
+      const int M = a.m_cur[s];
+      const int64_t doff = a.dict_off[s];
+      const double* Ws = a.W + a.w_off[s];
+      double* betas = a.beta + doff;
+      double* colsq = a.col_sq + doff;
+      const double lam1 = a.lam1[s], lam2 = a.lam2[s], tol = a.tol[s];
+      const int max_iters = a.max_iters[s];
+      __syncwarp();
+      for (int c = lane; c < M; c += 32) {
+        codes[c] = tile_code(a.tile_mask[doff + c]);
+        offs[c] = static_cast<int>(a.col_off[doff + c]);
+      }
+      __syncwarp();
+
+      double r[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int p = 64 * (k >> 1) + 2 * lane + (k & 1);
+        const int row = a.perm ? (p < N ? a.perm[r0 + p] : 0) : p;
+        r[k] = (p < N) ? a.y[r0 + row] : 0.0;
+      }
+
+      // ---- copy issue (lean kernel's ring; parameters from shared memory)
+      const int total = M * (1 + max_iters);
+      int issued = 0, next_col = 0;
+      auto issue_one = [&](double dep) {
+        if (lane == 0) {
+          const int code = codes[next_col];
+          const uint32_t bytes = static_cast<uint32_t>(code_tiles(code)) * 256u;
+          const uint32_t bar = bar_s + ist * 8;
+          if (bytes) {
+            mbar_expect_s(bar, bytes);
+            bulk_g2s_dep(ring_s + ist * (SLOT * 8), Ws + offs[next_col], bytes, bar, dep);
+          } else {
+            mbar_arrive_s(bar);
+          }
+        }
+        if (++ist == STAGES) ist = 0;
+        ++issued;
+        if (++next_col == M) next_col = 0;
+      };
+      for (int q = 0; q < STAGES && issued < total; ++q) issue_one(0.0);
+      int consumed = 0;
+      // next stream column -> w (run code of that column); refill its slot
+      auto take = [&](int col, double (&w)[R]) {
+        mbar_wait_s(bar_s + st * 8, ph);
+        const int code = codes[col];
+        const int a0 = code & 0xff, la = (code >> 8) & 0xff;
+        const uint32_t cA = ring_s + st * (SLOT * 8) + 16u * lane - 256u * a0;
+        const int hA = half - a0;
+        double dep = 0.0;
+#pragma unroll
+        for (int q = 0; q < R / 2; ++q) {
+          const bool inA = static_cast<unsigned>(hA + 2 * q) < static_cast<unsigned>(la);
+          lds_v2((inA ? cA : zero_s) + 512u * q, w[2 * q], w[2 * q + 1]);
+          dep += w[2 * q];
+        }
+        if (issued < total) issue_one(dep);
+        if (++st == STAGES) {
+          st = 0;
+          ph ^= 1u;
+        }
+        ++consumed;
+      };
+      auto dotp = [&](const double (&w)[R], const double (&x)[R]) {
+        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          if ((k & 3) == 0) d0 = fma(w[k], x[k], d0);
+          else if ((k & 3) == 1) d1 = fma(w[k], x[k], d1);
+          else if ((k & 3) == 2) d2 = fma(w[k], x[k], d2);
+          else d3 = fma(w[k], x[k], d3);
+        }
+        return (d0 + d1) + (d2 + d3);
+      };
+
+      double wA[R], wB[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) wA[k] = wB[k] = 0.0;  // an odd M leaves wB unloaded (multiplied by 0)
+      // ---- prologue: col_sq, r = y - W beta0, g_j = W_j . W_{j+1}
+      {
+        auto pro = [&](int j, double (&w)[R], const double (&wprev)[R]) {
+          take(j, w);
+          const double cs = warp_sum(dotp(w, w));
+          // consecutive-pair product g_{j-1} = W_{j-1} . W_j for pairs starting at even j-1
+          const double g = (j & 1) ? warp_sum(dotp(w, wprev)) : 0.0;
+          if (lane == 0) {
+            colsq[j] = cs;
+            if (j & 1) gn[j - 1] = g;
+          }
+          const double b0 = betas[j];
+          if (b0 != 0.0) {
+#pragma unroll
+            for (int k = 0; k < R; ++k) r[k] = fma(-b0, w[k], r[k]);
+          }
+        };
+        for (int j = 0; j < M; j += 2) {
+          pro(j, wA, wB);
+          if (j + 1 < M) pro(j + 1, wB, wA);
+        }
+      }
+      __syncwarp();
+
+      int sweeps_done = 0, conv = 0;
+      double obj = 0.0;
+      for (int sw = 0; sw < max_iters; ++sw) {
+        double max_delta = 0.0;
+        // column pairs (j, j+1): both dots against the same residual, both
+        // 5-level reductions interleaved, then the two soft thresholds in order
+        // with column j+1's dot corrected by d_j g_j, then both updates
+        for (int j = 0; j < M; j += 2) {
+          if ((j & 31) == 0) {
+            __syncwarp();
+            const int c = j + lane;
+            const double bv = c < M ? betas[c] : 0.0;
+            const double cv = c < M ? colsq[c] : 0.0;
+            pb[lane] = bv;
+            pc[lane] = cv;
+            const double dnv = __dadd_rn(cv, lam2);
+            pinv[lane] = dnv > 0.0 ? __ddiv_rn(1.0, dnv) : 0.0;
+            __syncwarp();
+          }
+          const bool two = j + 1 < M;
+          take(j, wA);
+          if (two) take(j + 1, wB);
+          double sA = dotp(wA, r);
+          double sB = two ? dotp(wB, r) : 0.0;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            sA += __shfl_xor_sync(0xffffffffu, sA, o);
+            sB += __shfl_xor_sync(0xffffffffu, sB, o);
+          }
+          const int t = j & 31;
+          auto solve = [&](int tt, double dot) {
+            const double b_old = pb[tt];
+            const double cs = pc[tt];
+            const double inv = pinv[tt];
+            const double dn = __dadd_rn(cs, lam2);
+            const double z = __dadd_rn(__dmul_rn(cs, b_old), dot);
+            const double np_ = __dsub_rn(z, lam1), nn_ = __dadd_rn(z, lam1);
+            const double qp = __dmul_rn(np_, inv), qn = __dmul_rn(nn_, inv);
+            const double bp = fma(fma(-qp, dn, np_), inv, qp);
+            const double bn = fma(fma(-qn, dn, nn_), inv, qn);
+            const double b_new = np_ > 0.0 ? bp : (nn_ < 0.0 ? bn : 0.0);
+            if (lane == 0) pb[tt] = b_new;
+            const double d = __dsub_rn(b_new, b_old);
+            const double ad = fabs(d);
+            max_delta = ad > max_delta ? ad : max_delta;
+            return d;
+          };
+          const double dA = solve(t, sA);
+          double dB = 0.0;
+          if (two) dB = solve(t + 1, __dsub_rn(sB, __dmul_rn(dA, gn[j])));
+#pragma unroll
+          for (int k = 0; k < R; ++k) r[k] = fma(-dB, wB[k], fma(-dA, wA[k], r[k]));
+          if (t + 2 >= 32 || j + 2 >= M) {  // chunk done: write its betas back
+            __syncwarp();
+            const int c = (j & ~31) + lane;
+            if (c < M && c <= j + 1) betas[c] = pb[lane];
+          }
+        }
+        __syncwarp();
+        double rss0 = 0.0, rss1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          if (k & 1) rss1 = fma(r[k], r[k], rss1);
+          else rss0 = fma(r[k], r[k], rss0);
+        }
+        double acc_l1 = 0.0, acc_l2 = 0.0, acc_max = 0.0;
+        for (int c = lane; c < M; c += 32) {
+          const double bl = betas[c];
+          const double ab = fabs(bl);
+          acc_l1 += ab;
+          acc_l2 = fma(bl, bl, acc_l2);
+          acc_max = fmax(acc_max, ab);
+        }
+        const double rss = warp_sum(rss0 + rss1);
+        const double l1 = warp_sum(acc_l1);
+        const double l2 = warp_sum(acc_l2);
+        const double mabs = warp_max(acc_max);
+        obj = __dadd_rn(__dadd_rn(__dmul_rn(0.5, rss), __dmul_rn(lam1, l1)),
+                        __dmul_rn(__dmul_rn(0.5, lam2), l2));
+        if (a.hist != nullptr && lane == 0) a.hist[a.hist_off[s] + sw] = obj;
+        sweeps_done = sw + 1;
+        if (max_delta <= __dmul_rn(tol, fmax(mabs, 1.0))) {
+          conv = 1;
+          break;
+        }
+      }
+      if (max_iters == 0) {
+        double rss = 0.0, l1 = 0.0, l2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < R; ++k) rss = fma(r[k], r[k], rss);
+        rss = warp_sum(rss);
+        for (int j = lane; j < M; j += 32) {
+          const double b = betas[j];
+          l1 += fabs(b);
+          l2 = fma(b, b, l2);
+        }
+        l1 = warp_sum(l1);
+        l2 = warp_sum(l2);
+        obj = __dadd_rn(__dadd_rn(__dmul_rn(0.5, rss), __dmul_rn(lam1, l1)),
+                        __dmul_rn(__dmul_rn(0.5, lam2), l2));
+      }
+      while (consumed < issued) {  // drain the prefetched columns of the sweep that will not run
+        mbar_wait_s(bar_s + st * 8, ph);
+        if (++st == STAGES) {
+          st = 0;
+          ph ^= 1u;
+        }
+        ++consumed;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        a.sweeps[s] = sweeps_done;
+        a.converged[s] = conv;
+        a.objective[s] = obj;
+      }
+    }
+    unsigned nxt = 0;
+    if (lane == 0) nxt = atomicAdd(&g_cd_queue, 1u) + total_warps;
+    item = __shfl_sync(0xffffffffu, nxt, 0);
+  }
+}
+
+template <int R, int STAGES, int WPC>
+int launch_cd_pipe(const CdArgs& a, int gcap, cudaStream_t stream) {
+  constexpr int SLOT = R * 32;
+  const size_t per_warp = static_cast<size_t>(STAGES) * SLOT * 8 + 96 * 8 + static_cast<size_t>(gcap) * 16;
+  const size_t smem = WPC * per_warp + static_cast<size_t>((WPC * STAGES + 1) & ~1) * 8 + SLOT * 8;
+  PAM_CUDA_CHECK(cudaFuncSetAttribute(cd_pipe_kernel<R, STAGES, WPC>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, sms = 148;
+  PAM_CUDA_CHECK(cudaGetDevice(&dev));
+  PAM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  void* qaddr = nullptr;
+  PAM_CUDA_CHECK(cudaGetSymbolAddress(&qaddr, g_cd_queue));
+  PAM_CUDA_CHECK(cudaMemsetAsync(qaddr, 0, sizeof(unsigned), stream));
+  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(sms, ceil_div(a.S, WPC)));
+  cd_pipe_kernel<R, STAGES, WPC><<<(unsigned)ctas, WPC * 32, smem, stream>>>(a, gcap);
+  PAM_LAUNCH_CHECK("cd_pipe_kernel");
+  return PAM_OK;
+}
+
 template <int R, int STAGES, int WPC, bool CPA, int RUNS>
 int launch_cd_tile_r(const CdArgs& a, cudaStream_t stream);
 
@@ -979,6 +1281,59 @@ int cd_dispatch(const CdArgs& a, int max_rows, cudaStream_t stream) {
   return PAM_ERR_UNSUPPORTED;
 }
 
+__global__ void max_m_kernel(int64_t S, const int64_t* order, const int32_t* m_cur, int* out) {
+  int m = 0;
+  for (int64_t i = threadIdx.x; i < S; i += blockDim.x) m = max(m, m_cur[order ? order[i] : i]);
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ int part[32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = max(m, part[w]);
+    *out = m;
+  }
+}
+
+// Few fits per SM (BASELINE configs 2-3, 64-256 fits): the software-pipelined
+// kernel.  PAM_CD_PIPE = 0 disables it, 1 forces it (257-1024 rows).
+int maybe_cd_pipe(const CdArgs& a, int max_rows, cudaStream_t stream, bool* used) {
+  *used = false;
+  const char* env = getenv("PAM_CD_PIPE");
+  const int mode = env ? atoi(env) : -1;
+  if (mode == 0 || max_rows <= 256 || max_rows > 1024 || tile_runs() != 1) return PAM_OK;
+  int dev = 0, sms = 148;
+  PAM_CUDA_CHECK(cudaGetDevice(&dev));
+  PAM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (mode != 1 && a.S > 3LL * sms) return PAM_OK;
+  // the per-warp staging holds a fit's run codes, offsets and consecutive-
+  // column products: size it from the largest dictionary of the batch
+  static int* d_m = nullptr;
+  if (!d_m) PAM_CUDA_CHECK(cudaMalloc(&d_m, sizeof(int)));
+  max_m_kernel<<<1, 1024, 0, stream>>>(a.S, a.order, a.m_cur, d_m);
+  PAM_LAUNCH_CHECK("max_m_kernel");
+  int max_m = 0;
+  PAM_CUDA_CHECK(cudaMemcpyAsync(&max_m, d_m, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  PAM_CUDA_CHECK(cudaStreamSynchronize(stream));
+  const int gcap = (max_m + 31) / 32 * 32;
+  const int wpc_need = static_cast<int>(std::min<int64_t>(3, std::max<int64_t>(1, ceil_div(a.S, sms))));
+  // shared memory per warp: 3 slots + params + 16 B per dictionary slot
+  const int R = max_rows <= 512 ? 16 : 32;
+  const size_t per_warp = 3 * R * 32 * 8 + 96 * 8 + static_cast<size_t>(gcap) * 16;
+  const size_t avail = 227 * 1024 - R * 32 * 8 - 64;
+  const int wpc_fit = static_cast<int>(avail / per_warp);
+  if (wpc_fit < 1) return PAM_OK;  // dictionary too large for the staging
+  const int wpc = std::min(wpc_need, wpc_fit);
+  *used = true;
+  if (R == 16) {
+    if (wpc >= 3) return launch_cd_pipe<16, 3, 3>(a, gcap, stream);
+    if (wpc == 2) return launch_cd_pipe<16, 3, 2>(a, gcap, stream);
+    return launch_cd_pipe<16, 3, 1>(a, gcap, stream);
+  }
+  if (wpc >= 3) return launch_cd_pipe<32, 3, 3>(a, gcap, stream);
+  if (wpc == 2) return launch_cd_pipe<32, 3, 2>(a, gcap, stream);
+  return launch_cd_pipe<32, 3, 1>(a, gcap, stream);
+}
+
 int cd_dispatch_tiles(const CdArgs& a, int max_rows, cudaStream_t stream) {
   // one warp per subdomain; tile k of a column <-> register r[k] of every lane.
   // PAM_CD_LEAN: 1 (default) lean kernel with TMA staging; 3 lean kernel with
@@ -986,6 +1341,11 @@ int cd_dispatch_tiles(const CdArgs& a, int max_rows, cudaStream_t stream) {
   // lean kernels need masks of <= 2 runs (PAM_TILE_RUNS != 0).
   const char* lean_env = getenv("PAM_CD_LEAN");
   const int lean = (tile_runs() == 0) ? 0 : (lean_env ? atoi(lean_env) : 1);
+  if (lean == 1) {
+    bool used = false;
+    const int rc = maybe_cd_pipe(a, max_rows, stream, &used);
+    if (used || rc != PAM_OK) return rc;
+  }
   if (lean == 3 && max_rows > 32 && max_rows <= 512) {
     if (max_rows <= 64) return launch_cd_tile<2, 4, 16, true>(a, stream);
     if (max_rows <= 128) return launch_cd_tile<4, 4, 16, true>(a, stream);

@@ -406,3 +406,27 @@ def test_config1_convergent_solver_matches_reference(cuda, golden):
         assert np.max(np.abs(sur.locals[s].beta - ref)) <= 1e-8 * max(1.0, np.abs(ref).max())
         obj = rep.rounds[s][0].objective
         assert abs(obj - float(g[f"s{s}_objective"])) <= 1e-8 * max(abs(float(g[f"s{s}_objective"])), 1e-300)
+
+
+@pytest.mark.parametrize("cells,px", [((32, 32), 1), ((24, 24), 2), ((40, 30), 1)])
+def test_pipelined_few_fit_kernel_matches_lean(cuda, monkeypatch, cells, px):
+    """The software-pipelined CD for few fits (lag-1 Gram correction, cd.cu
+    cd_pipe_kernel) against the lean per-column kernel: same dictionaries,
+    sweeps within one, beta and objectives ~1e-12 (only dot-product rounding
+    differs)."""
+    field = pam.box_field_2d(*cells)
+    part = pam.make_partition(field.mesh, px, 1)
+    cfg = pam.AdaptiveConfig(k_top=24, m_max=150, m_q=3, max_rounds=3, elastic=EN_2D,
+                             offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
+    spec = pam.DictionarySpec(sigma=0.5 / cells[0])
+    monkeypatch.setenv("PAM_CD_PIPE", "0")
+    lean, rl = pam.fit_parallel(field, part, cfg, spec)
+    monkeypatch.setenv("PAM_CD_PIPE", "1")
+    pipe, rp = pam.fit_parallel(field, part, cfg, spec)
+    for a, b in zip(lean.locals, pipe.locals):
+        np.testing.assert_array_equal(a.dictionary.centers, b.dictionary.centers)
+        assert np.max(np.abs(a.beta - b.beta)) <= 1e-10 * max(1, np.abs(a.beta).max())
+    for ra, rb in zip(rl.rounds, rp.rounds):
+        for x, y in zip(ra, rb):
+            assert (x.centers, x.added) == (y.centers, y.added)
+            assert abs(x.objective - y.objective) <= 1e-10 * abs(x.objective)
