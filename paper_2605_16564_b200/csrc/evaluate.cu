@@ -22,13 +22,14 @@
 #include <string.h>
 
 #include <algorithm>
+#include <type_traits>
 
 namespace pam {
 
-template <int D>
+template <int D, typename IdxT>
 __global__ void locate_kernel(int64_t P, const double* __restrict__ pts,
                               const int32_t* __restrict__ shape, const double* __restrict__ edges,
-                              int64_t* __restrict__ owner, int64_t* err) {
+                              IdxT* __restrict__ owner, int64_t* err) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < P;
        j += (int64_t)gridDim.x * blockDim.x) {
     int64_t own = 0, stride = 1;
@@ -55,41 +56,46 @@ __global__ void locate_kernel(int64_t P, const double* __restrict__ pts,
       report_error(err, PAM_ERR_OUTSIDE, j);
       own = -1;
     }
-    owner[j] = own;
+    owner[j] = static_cast<IdxT>(own);
   }
 }
 
-__global__ void histogram_kernel(int64_t P, const int64_t* __restrict__ owner,
-                                 unsigned long long* __restrict__ counts) {
+// unsigned counterpart for atomicAdd (int32 -> unsigned, int64 -> unsigned long long)
+template <typename IdxT>
+using UIdx = std::conditional_t<sizeof(IdxT) == 8, unsigned long long, unsigned int>;
+
+template <typename IdxT>
+__global__ void histogram_kernel(int64_t P, const IdxT* __restrict__ owner, IdxT* __restrict__ counts) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < P;
        j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t o = owner[j];
-    if (o >= 0) atomicAdd(&counts[o], 1ull);
+    const IdxT o = owner[j];
+    if (o >= 0) atomicAdd(reinterpret_cast<UIdx<IdxT>*>(&counts[o]), 1u);
   }
 }
 
-// exclusive scan over S counts, single CTA (S up to a few 1e5)
+// exclusive scan over S counts, single CTA (S up to a few 1e5); start[S] =
+// number of located points (the evaluation's sorted length)
 constexpr int SCAN_THREADS = 1024;
+template <typename IdxT>
 __global__ void __launch_bounds__(SCAN_THREADS)
-scan_kernel(int64_t S, const unsigned long long* __restrict__ counts,
-            unsigned long long* __restrict__ start, unsigned long long* __restrict__ cursor) {
-  __shared__ unsigned long long part[SCAN_THREADS];
+scan_kernel(int64_t S, const IdxT* __restrict__ counts, IdxT* __restrict__ start, IdxT* __restrict__ cursor) {
+  __shared__ IdxT part[SCAN_THREADS];
   const int64_t per = (S + SCAN_THREADS - 1) / SCAN_THREADS;
   const int64_t lo = threadIdx.x * per, hi = min(S, lo + per);
-  unsigned long long acc = 0;
+  IdxT acc = 0;
   for (int64_t i = lo; i < hi; ++i) acc += counts[i];
   part[threadIdx.x] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned long long run = 0;
+    IdxT run = 0;
     for (int k = 0; k < SCAN_THREADS; ++k) {
-      const unsigned long long v = part[k];
+      const IdxT v = part[k];
       part[k] = run;
       run += v;
     }
   }
   __syncthreads();
-  unsigned long long run = part[threadIdx.x];
+  IdxT run = part[threadIdx.x];
   for (int64_t i = lo; i < hi; ++i) {
     start[i] = run;
     cursor[i] = run;
@@ -98,15 +104,16 @@ scan_kernel(int64_t S, const unsigned long long* __restrict__ counts,
   if (threadIdx.x == SCAN_THREADS - 1) start[S] = run;  // last range ends at the total
 }
 
-__global__ void scatter_kernel(int64_t P, const int64_t* __restrict__ owner,
-                               unsigned long long* __restrict__ cursor, int64_t* __restrict__ perm,
-                               int64_t* __restrict__ sorted_owner) {
+template <typename IdxT>
+__global__ void scatter_kernel(int64_t P, const IdxT* __restrict__ owner, IdxT* __restrict__ cursor,
+                               IdxT* __restrict__ perm, IdxT* __restrict__ sorted_owner) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < P;
        j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t o = owner[j];
+    const IdxT o = owner[j];
     if (o < 0) continue;
-    const unsigned long long pos = atomicAdd(&cursor[o], 1ull);
-    perm[pos] = j;
+    const IdxT pos = static_cast<IdxT>(
+        atomicAdd(reinterpret_cast<UIdx<IdxT>*>(&cursor[o]), 1u));
+    perm[pos] = static_cast<IdxT>(j);
     sorted_owner[pos] = o;
   }
 }
@@ -222,10 +229,11 @@ __device__ double shepard_exact_point(const double* x, const double* centres, co
 // sorted_owner == nullptr: single-dictionary mode (LocalSurrogate.evaluate /
 // shepard_eval, rbf.py:152-192): every point belongs to dictionary 0 of
 // size single_m, log transform = single_exp.  perm == nullptr: identity.
-template <int D, int PT, bool REPL>
+template <int D, int PT, bool REPL, typename IdxT>
 __global__ void __launch_bounds__(EVAL_WARPS * 32)
-eval_kernel(int64_t P, const double* __restrict__ pts, const int64_t* __restrict__ perm,
-            const int64_t* __restrict__ sorted_owner, const int64_t* __restrict__ dict_off,
+eval_kernel(int64_t P, const double* __restrict__ pts, const IdxT* __restrict__ perm,
+            const IdxT* __restrict__ sorted_owner, const IdxT* __restrict__ n_sorted,
+            const int64_t* __restrict__ dict_off,
             const int32_t* __restrict__ m_cur, const double* __restrict__ centres,
             const double* __restrict__ widths, const double* __restrict__ beta,
             const int32_t* __restrict__ log_flag, int single_m, int single_exp,
@@ -241,6 +249,9 @@ eval_kernel(int64_t P, const double* __restrict__ pts, const int64_t* __restrict
   const int lane = threadIdx.x & 31;
   const int rep = lane & (XR_REP - 1);
   double* const st = stage[warp];
+  // sorted mode: only the located points were sorted (start[S]); the rest is
+  // the error path (the caller raises)
+  if (n_sorted) P = static_cast<int64_t>(*n_sorted);
   const int64_t n_tiles = (P + 32 * PT - 1) / (32 * PT);
   // persistent warps pulling 32*PT-point tiles from a queue counter in the
   // caller's workspace (balanced whatever the owner-run mix of a tile and
@@ -262,8 +273,8 @@ eval_kernel(int64_t P, const double* __restrict__ pts, const int64_t* __restrict
     for (int p = 0; p < PT; ++p) {
       const int64_t pos = base + 32 * p + lane;
       have[p] = pos < P;
-      own[p] = have[p] ? (sorted_owner ? sorted_owner[pos] : 0) : INT64_MAX;
-      idx[p] = have[p] ? (perm ? perm[pos] : pos) : 0;
+      own[p] = have[p] ? (sorted_owner ? static_cast<int64_t>(sorted_owner[pos]) : 0) : INT64_MAX;
+      idx[p] = have[p] ? (perm ? static_cast<int64_t>(perm[pos]) : pos) : 0;
 #pragma unroll
       for (int k = 0; k < D; ++k) x[p][k] = have[p] ? pts[idx[p] * D + k] : 0.0;
     }
@@ -385,9 +396,9 @@ int ensure_exp2_table() {
   return PAM_OK;
 }
 
-template <int D, int PT, bool REPL>
-int launch_eval_v(cudaStream_t st, int64_t P, const double* pts, const int64_t* perm,
-                  const int64_t* sorted_owner, const int64_t* dict_off, const int32_t* m_cur,
+template <int D, int PT, bool REPL, typename IdxT>
+int launch_eval_v(cudaStream_t st, int64_t P, const double* pts, const IdxT* perm,
+                  const IdxT* sorted_owner, const IdxT* n_sorted, const int64_t* dict_off, const int32_t* m_cur,
                   const double* centres, const double* widths, const double* beta,
                   const int32_t* log_flag, int single_m, int single_exp, double* out, int64_t* err,
                   unsigned long long* queue) {
@@ -398,9 +409,9 @@ int launch_eval_v(cudaStream_t st, int64_t P, const double* pts, const int64_t* 
     PAM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     // maximum shared-memory carve-out, so the occupancy the grid is sized for
     // is the one the SM actually grants
-    PAM_CUDA_CHECK(cudaFuncSetAttribute(eval_kernel<D, PT, REPL>,
+    PAM_CUDA_CHECK(cudaFuncSetAttribute(eval_kernel<D, PT, REPL, IdxT>,
                                         cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    PAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eval_kernel<D, PT, REPL>,
+    PAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eval_kernel<D, PT, REPL, IdxT>,
                                                                  EVAL_WARPS * 32, 0));
     grid_cap = sms * std::max(per_sm, 1);
   }
@@ -409,29 +420,29 @@ int launch_eval_v(cudaStream_t st, int64_t P, const double* pts, const int64_t* 
   const int64_t ctas = queue ? std::min<int64_t>(grid_cap, tiles_ctas) : tiles_ctas;
   if (ctas > 0x7fffffffLL) return PAM_ERR_ARG;
   if (queue) PAM_CUDA_CHECK(cudaMemsetAsync(queue, 0, sizeof(unsigned long long), st));
-  eval_kernel<D, PT, REPL><<<(unsigned)ctas, EVAL_WARPS * 32, 0, st>>>(
-      P, pts, perm, sorted_owner, dict_off, m_cur, centres, widths, beta, log_flag, single_m,
+  eval_kernel<D, PT, REPL, IdxT><<<(unsigned)ctas, EVAL_WARPS * 32, 0, st>>>(
+      P, pts, perm, sorted_owner, n_sorted, dict_off, m_cur, centres, widths, beta, log_flag, single_m,
       single_exp, out, err, queue);
   PAM_LAUNCH_CHECK("eval_kernel");
   return PAM_OK;
 }
 
-template <int D>
-int launch_eval(cudaStream_t st, int64_t P, const double* pts, const int64_t* perm,
-                const int64_t* sorted_owner, const int64_t* dict_off, const int32_t* m_cur,
+template <int D, typename IdxT>
+int launch_eval(cudaStream_t st, int64_t P, const double* pts, const IdxT* perm,
+                const IdxT* sorted_owner, const IdxT* n_sorted, const int64_t* dict_off, const int32_t* m_cur,
                 const double* centres, const double* widths, const double* beta,
                 const int32_t* log_flag, int single_m, int single_exp, double* out, int64_t* err,
                 unsigned long long* queue) {
   const int rc = ensure_exp2_table();
   if (rc != PAM_OK) return rc;
-#define PAM_EVAL_ARGS st, P, pts, perm, sorted_owner, dict_off, m_cur, centres, widths, beta, log_flag, \
+#define PAM_EVAL_ARGS st, P, pts, perm, sorted_owner, n_sorted, dict_off, m_cur, centres, widths, beta, log_flag, \
                       single_m, single_exp, out, err, queue
   if (eval_pt() == 4) {
-    if (eval_repl()) return launch_eval_v<D, 4, true>(PAM_EVAL_ARGS);
-    return launch_eval_v<D, 4, false>(PAM_EVAL_ARGS);
+    if (eval_repl()) return launch_eval_v<D, 4, true, IdxT>(PAM_EVAL_ARGS);
+    return launch_eval_v<D, 4, false, IdxT>(PAM_EVAL_ARGS);
   }
-  if (eval_repl()) return launch_eval_v<D, 2, true>(PAM_EVAL_ARGS);
-  return launch_eval_v<D, 2, false>(PAM_EVAL_ARGS);
+  if (eval_repl()) return launch_eval_v<D, 2, true, IdxT>(PAM_EVAL_ARGS);
+  return launch_eval_v<D, 2, false, IdxT>(PAM_EVAL_ARGS);
 #undef PAM_EVAL_ARGS
 }
 
@@ -455,12 +466,56 @@ extern "C" int pam_locate_f64(int dim, int64_t P, const double* pts, const int32
   if (P == 0) return PAM_OK;
   cudaStream_t st = as_stream(stream);
   const int g = grid_for(P, 256);
-  if (dim == 1) locate_kernel<1><<<g, 256, 0, st>>>(P, pts, shape, edges, owner, err);
-  else if (dim == 2) locate_kernel<2><<<g, 256, 0, st>>>(P, pts, shape, edges, owner, err);
-  else locate_kernel<3><<<g, 256, 0, st>>>(P, pts, shape, edges, owner, err);
+  if (dim == 1) locate_kernel<1, int64_t><<<g, 256, 0, st>>>(P, pts, shape, edges, owner, err);
+  else if (dim == 2) locate_kernel<2, int64_t><<<g, 256, 0, st>>>(P, pts, shape, edges, owner, err);
+  else locate_kernel<3, int64_t><<<g, 256, 0, st>>>(P, pts, shape, edges, owner, err);
   PAM_LAUNCH_CHECK("locate_kernel");
   return PAM_OK;
 }
+
+namespace pam {
+// locate -> counting sort by owner -> evaluation, with IdxT-wide indices
+// (int32 whenever P and S fit: half the sort traffic and 32-bit atomics)
+template <typename IdxT>
+int eval_pipeline(int dim, int64_t P, const double* pts, const int32_t* shape, const double* edges,
+                  int64_t S, const int64_t* dict_off, const int32_t* m_cur, const double* centres,
+                  const double* widths, const double* beta, const int32_t* log_flag, double* out,
+                  void* work, int64_t* err, cudaStream_t st) {
+  char* w = static_cast<char*>(work);
+  IdxT* owner = reinterpret_cast<IdxT*>(w);
+  IdxT* perm = owner + P;
+  IdxT* sorted_owner = perm + P;
+  IdxT* counts = sorted_owner + P;
+  IdxT* cursor = counts + S;
+  IdxT* start = cursor + S;
+  // the tile-queue counter, 8-byte aligned after start[S]
+  unsigned long long* queue = reinterpret_cast<unsigned long long*>(
+      (reinterpret_cast<uintptr_t>(start + S + 1) + 7) & ~static_cast<uintptr_t>(7));
+  const int g = grid_for(P, 256);
+  if (dim == 1) locate_kernel<1, IdxT><<<g, 256, 0, st>>>(P, pts, shape, edges, owner, err);
+  else if (dim == 2) locate_kernel<2, IdxT><<<g, 256, 0, st>>>(P, pts, shape, edges, owner, err);
+  else locate_kernel<3, IdxT><<<g, 256, 0, st>>>(P, pts, shape, edges, owner, err);
+  PAM_LAUNCH_CHECK("locate_kernel");
+  PAM_CUDA_CHECK(cudaMemsetAsync(counts, 0, S * sizeof(IdxT), st));
+  histogram_kernel<IdxT><<<g, 256, 0, st>>>(P, owner, counts);
+  PAM_LAUNCH_CHECK("histogram_kernel");
+  scan_kernel<IdxT><<<1, SCAN_THREADS, 0, st>>>(S, counts, start, cursor);
+  PAM_LAUNCH_CHECK("scan_kernel");
+  // points that failed to locate are not scattered: the evaluation covers
+  // the start[S] located ones (error path: the caller raises)
+  scatter_kernel<IdxT><<<g, 256, 0, st>>>(P, owner, cursor, perm, sorted_owner);
+  PAM_LAUNCH_CHECK("scatter_kernel");
+  const IdxT* n_sorted = start + S;
+  if (dim == 1)
+    return launch_eval<1, IdxT>(st, P, pts, perm, sorted_owner, n_sorted, dict_off, m_cur, centres, widths,
+                                beta, log_flag, 0, 0, out, err, queue);
+  if (dim == 2)
+    return launch_eval<2, IdxT>(st, P, pts, perm, sorted_owner, n_sorted, dict_off, m_cur, centres, widths,
+                                beta, log_flag, 0, 0, out, err, queue);
+  return launch_eval<3, IdxT>(st, P, pts, perm, sorted_owner, n_sorted, dict_off, m_cur, centres, widths,
+                              beta, log_flag, 0, 0, out, err, queue);
+}
+}  // namespace pam
 
 extern "C" int pam_eval_f64(int dim, int64_t P, const double* pts, const int32_t* shape,
                             const double* edges, int64_t S, const int64_t* dict_off,
@@ -470,36 +525,11 @@ extern "C" int pam_eval_f64(int dim, int64_t P, const double* pts, const int32_t
   if (dim < 1 || dim > 3 || P < 0 || S < 1 || !work) return PAM_ERR_ARG;
   if (P == 0) return PAM_OK;
   cudaStream_t st = as_stream(stream);
-  char* w = static_cast<char*>(work);
-  int64_t* owner = reinterpret_cast<int64_t*>(w);
-  int64_t* perm = owner + P;
-  int64_t* sorted_owner = perm + P;
-  unsigned long long* counts = reinterpret_cast<unsigned long long*>(sorted_owner + P);
-  unsigned long long* cursor = counts + S;
-  unsigned long long* start = cursor + S;
-  unsigned long long* queue = start + S + 1;  // in the workspace slack
-  int rc = pam_locate_f64(dim, P, pts, shape, edges, owner, err, stream);
-  if (rc != PAM_OK) return rc;
-  PAM_CUDA_CHECK(cudaMemsetAsync(counts, 0, S * sizeof(unsigned long long), st));
-  const int g = grid_for(P, 256);
-  histogram_kernel<<<g, 256, 0, st>>>(P, owner, counts);
-  PAM_LAUNCH_CHECK("histogram_kernel");
-  scan_kernel<<<1, SCAN_THREADS, 0, st>>>(S, counts, start, cursor);
-  PAM_LAUNCH_CHECK("scan_kernel");
-  // points that failed to locate are not scattered; pad the tail so every
-  // sorted slot is defined (error path only: the caller raises).
-  PAM_CUDA_CHECK(cudaMemsetAsync(sorted_owner, 0, P * sizeof(int64_t), st));
-  PAM_CUDA_CHECK(cudaMemsetAsync(perm, 0, P * sizeof(int64_t), st));
-  scatter_kernel<<<g, 256, 0, st>>>(P, owner, cursor, perm, sorted_owner);
-  PAM_LAUNCH_CHECK("scatter_kernel");
-  if (dim == 1)
-    return launch_eval<1>(st, P, pts, perm, sorted_owner, dict_off, m_cur, centres, widths, beta,
-                          log_flag, 0, 0, out, err, queue);
-  if (dim == 2)
-    return launch_eval<2>(st, P, pts, perm, sorted_owner, dict_off, m_cur, centres, widths, beta,
-                          log_flag, 0, 0, out, err, queue);
-  return launch_eval<3>(st, P, pts, perm, sorted_owner, dict_off, m_cur, centres, widths, beta,
-                        log_flag, 0, 0, out, err, queue);
+  if (P < 0x7fffffffLL && S < 0x7fffffffLL)
+    return eval_pipeline<int32_t>(dim, P, pts, shape, edges, S, dict_off, m_cur, centres, widths, beta,
+                                  log_flag, out, work, err, st);
+  return eval_pipeline<int64_t>(dim, P, pts, shape, edges, S, dict_off, m_cur, centres, widths, beta,
+                                log_flag, out, work, err, st);
 }
 
 extern "C" int pam_shepard_eval_f64(int dim, int64_t P, const double* pts, int64_t M,
@@ -511,11 +541,11 @@ extern "C" int pam_shepard_eval_f64(int dim, int64_t P, const double* pts, int64
   cudaStream_t st = as_stream(stream);
   const int m = static_cast<int>(M);
   if (dim == 1)
-    return launch_eval<1>(st, P, pts, nullptr, nullptr, nullptr, nullptr, centres, widths, beta,
+    return launch_eval<1, int64_t>(st, P, pts, nullptr, nullptr, nullptr, nullptr, nullptr, centres, widths, beta,
                           nullptr, m, exp_out, out, err, nullptr);
   if (dim == 2)
-    return launch_eval<2>(st, P, pts, nullptr, nullptr, nullptr, nullptr, centres, widths, beta,
+    return launch_eval<2, int64_t>(st, P, pts, nullptr, nullptr, nullptr, nullptr, nullptr, centres, widths, beta,
                           nullptr, m, exp_out, out, err, nullptr);
-  return launch_eval<3>(st, P, pts, nullptr, nullptr, nullptr, nullptr, centres, widths, beta,
+  return launch_eval<3, int64_t>(st, P, pts, nullptr, nullptr, nullptr, nullptr, nullptr, centres, widths, beta,
                         nullptr, m, exp_out, out, err, nullptr);
 }
