@@ -774,6 +774,9 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
       fetch_params(0);
       int sweeps_done = 0, conv = 0;
       double obj = 0.0;
+#ifdef PAM_CD_PAD
+      unsigned pad0 = lane, pad1 = lane + 1, pad2 = lane + 2, pad3 = lane + 3;
+#endif
       for (int sw = 0; sw < max_iters; ++sw) {
         double max_delta = 0.0, acc_l1 = 0.0, acc_l2 = 0.0, acc_max = 0.0;
         for (int cb = 0; cb < M; cb += 32) {
@@ -824,6 +827,17 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
             if (lane == 0) pb[t] = b_new;
             const double ad = fabs(d);
             max_delta = ad > max_delta ? ad : max_delta;  // fmax without the NaN fix-up
+#ifdef PAM_CD_PAD
+            // diagnostic build (-DPAM_CD_PAD=n): n independent,
+            // non-foldable integer instructions per column
+#pragma unroll
+            for (int u = 0; u < PAM_CD_PAD / 4; ++u) {
+              pad0 = pad0 * pad0 + (2u * u + 1u);
+              pad1 = pad1 * pad1 + (2u * u + 3u);
+              pad2 = pad2 * pad2 + (2u * u + 5u);
+              pad3 = pad3 * pad3 + (2u * u + 7u);
+            }
+#endif
           }
           __syncwarp();
           if (lane < nc) {
@@ -870,6 +884,9 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
         obj = __dadd_rn(__dadd_rn(__dmul_rn(0.5, rss), __dmul_rn(lam1, l1)),
                         __dmul_rn(__dmul_rn(0.5, lam2), l2));
       }
+#ifdef PAM_CD_PAD
+      if ((pad0 ^ pad1 ^ pad2 ^ pad3) == 0x12345679u) a.sweeps[0] = -1;  // keeps the padding live
+#endif
       // drain the prefetched columns of the sweep that will not run
       if (CPA) {
         cp_async_wait<0>();
