@@ -10,9 +10,10 @@
 //      edges, so ownership is bit-exact.  Points outside every
 //      box report the FIRST offending index (atomicMin).
 //   2. counting sort of point ids by owner (histogram, exclusive scan,
-//      scatter) so each subdomain's dictionary is read once per 64-point
-//      warp tile (from L2) and served to the warp from shared memory.
-//   3. eval: one warp per 64 sorted points, per owner run the one-pass
+//      scatter; 32-bit indices when P and S fit) so each subdomain's
+//      dictionary is read once per 128-point warp tile (from L2) and served
+//      to the warp from shared memory.
+//   3. eval: one warp per 128 sorted points (4 per lane), per owner run the one-pass
 //      Shepard sum with a table-driven FP64 exp (below); exp() of the blend
 //      when log_transform; results scattered back to input order.
 //
