@@ -200,7 +200,11 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_gram_kernel(const GramArgs a) 
         if (lane == 0) {
           const int c0 = next_group * cps;
           const int nc = min(cps, M - c0);
-          const uint32_t nb = static_cast<uint32_t>(nc) * ldgs * sizeof(double);
+          // one column per slot: copy only the current M entries (even, for the
+          // 16-byte size rule) -- the leading dimension may exceed the slot
+          // for wide dictionaries that grow across rounds
+          const uint32_t nb = (cps == 1 ? static_cast<uint32_t>((M + 1) & ~1)
+                                        : static_cast<uint32_t>(nc) * ldgs) * sizeof(double);
           const uint32_t bar = bar_s + ist * 8;
           mbar_expect_s(bar, nb);
           bulk_g2s_dep(ring_s + ist * (SLOT * 8), Gs + (int64_t)c0 * ldgs, nb, bar, dep);
@@ -433,6 +437,14 @@ extern "C" int pam_cd_gram_f64(int64_t S, const int64_t* order, const int64_t* d
   if (max_m <= 128) return launch_gram_cd<4, 3, 16, 512>(a, st);
   if (max_m <= 256) return launch_gram_cd<8, 3, 16, 512>(a, st);
   if (max_m <= 512) return launch_gram_cd<16, 3, 16, 512>(a, st);
-  set_last_error("pam_cd_gram_f64: Gram-form CD supports M <= 512 (use the residual form)");
+  // wide dictionaries, chosen by the host only for batches of few fits (one
+  // per SM), where the residual form is bound by one fit's per-column chain:
+  // c in up to 192 registers, one warp per CTA (= per SM) with an 8-deep ring
+  // of G columns (up to 196 KB in flight: one SM must pull ~100 GB/s)
+  if (max_m <= 1024) return launch_gram_cd<32, 8, 1, 1024>(a, st);
+  if (max_m <= 2048) return launch_gram_cd<64, 8, 1, 2048>(a, st);
+  if (max_m <= 2304) return launch_gram_cd<72, 8, 1, 2304>(a, st);
+  if (max_m <= 3072) return launch_gram_cd<96, 8, 1, 3072>(a, st);
+  set_last_error("pam_cd_gram_f64: Gram-form CD supports M <= 3072 (use the residual form)");
   return PAM_ERR_UNSUPPORTED;
 }

@@ -183,25 +183,48 @@ def rcb_permutation(points: np.ndarray, leaf: int = 32) -> np.ndarray:
 
 
 GRAM_MAX_M = 512
+GRAM_WIDE_MAX_M = 3072  # covariance form for few-fit batches (gram.cu wide configurations)
+
+
+def _sm_count() -> int:
+    try:
+        torch = nat.torch_mod()
+        if torch.cuda.is_available():
+            return int(torch.cuda.get_device_properties(0).multi_processor_count)
+    except Exception:  # noqa: BLE001 - host-only use (tests): B200's count
+        pass
+    return 148
 
 
 def cd_form(n_rows, cap) -> str:
-    """Which CD formulation streams fewer bytes for this batch.
+    """Which CD formulation is faster for this batch.
 
     Residual form streams N*M doubles per sweep, the covariance (Gram) form
-    M*M (hard part 1); the Gram kernel keeps c in registers and
-    supports M <= 512.  Env PAM_CD_FORM = auto | residual | gram.
+    M*M (hard part 1).  Many fits: the form that streams fewer
+    bytes (Gram needs M <= 512 and cap <= 0.75 N).  Few fits (at most one per
+    SM, e.g. BASELINE config 2): the residual form is bound by one fit's
+    per-column dependency chain (~0.55 us per column) while the
+    covariance form's chain is ~0.12 us per coordinate, so it wins whenever
+    its M*M stream still fits the HBM time (M <= 3072).  Env PAM_CD_FORM =
+    auto | residual | gram.
     """
     import os
 
     forced = os.environ.get("PAM_CD_FORM", "auto")
     cap = np.asarray(cap, dtype=np.int64)
-    fits = int(cap.max()) <= GRAM_MAX_M
-    if forced == "gram" and fits:
+    cmax = int(cap.max())
+    if forced == "gram" and cmax <= GRAM_WIDE_MAX_M:
         return "gram"
-    if forced == "residual" or not fits:
+    if forced == "residual":
         return "residual"
-    return "gram" if np.all(cap * 4 <= np.asarray(n_rows) * 3) else "residual"
+    if cmax <= GRAM_MAX_M and np.all(cap * 4 <= np.asarray(n_rows) * 3):
+        return "gram"
+    if cap.size <= _sm_count() and cmax <= GRAM_WIDE_MAX_M:
+        t_res = cmax * 0.55e-6                                   # per sweep, chain-bound
+        t_gram = max(cmax * 0.12e-6, float(np.sum(cap.astype(np.float64) ** 2)) * 8 / 6.5e12)
+        if t_gram < 0.7 * t_res:
+            return "gram"
+    return "residual"
 
 
 def device_bytes(n_rows, cap) -> np.ndarray:

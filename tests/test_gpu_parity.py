@@ -217,6 +217,7 @@ def test_fit_parallel_deterministic_and_chunk_independent(cuda, monkeypatch):
 def test_tile_packed_stream_matches_dense(cuda, monkeypatch, cells, tau):
     """Tile-dropping (tau = 2^-100 and the default 1e-16) vs exact dense streaming:
     same decisions, beta ~1e-12."""
+    monkeypatch.setenv("PAM_CD_FORM", "residual")  # few fits would pick the covariance form
     field = pam.box_field_2d(*cells)
     part = pam.make_partition(field.mesh, 2, 2)
     cfg = pam.AdaptiveConfig(k_top=cells[0], m_max=6 * cells[0], m_q=3, max_rounds=3, elastic=EN_2D,
@@ -243,6 +244,7 @@ def test_cd_staging_variants_match(cuda, monkeypatch, variant):
     """Opt-in CD variants (byte ring, LDGSTS staging, generic tile kernel, per-lane
     cp.async staging, two-run / exact tile masks, 4-slot ring) reproduce the default
     lean kernel."""
+    monkeypatch.setenv("PAM_CD_FORM", "residual")  # few fits would pick the covariance form
     field = pam.box_field_2d(40, 40)
     part = pam.make_partition(field.mesh, 2, 2)  # 400 rows: the R=16 tile kernels
     cfg = pam.AdaptiveConfig(k_top=40, m_max=240, m_q=3, max_rounds=3, elastic=EN_2D,
@@ -368,6 +370,7 @@ def test_sharded_fit_single_rank_device_path(cuda):
 @pytest.mark.parametrize("cells", [(20, 20), (30, 30)])
 def test_lean_kernel_small_rows_odd_columns(cuda, monkeypatch, cells):
     """Lean CD at R=4 / R=8 with odd dictionary sizes and ragged batches == the generic kernel."""
+    monkeypatch.setenv("PAM_CD_FORM", "residual")  # few fits would pick the covariance form
     field = pam.box_field_2d(*cells)
     part = pam.make_partition(field.mesh, 2, 2)  # 100 / 225 rows
     cfg = pam.AdaptiveConfig(k_top=7, m_max=60, m_q=3, max_rounds=3, elastic=EN_2D,
@@ -414,6 +417,7 @@ def test_pipelined_few_fit_kernel_matches_lean(cuda, monkeypatch, cells, px):
     cd_pipe_kernel) against the lean per-column kernel: same dictionaries,
     sweeps within one, beta and objectives ~1e-12 (only dot-product rounding
     differs)."""
+    monkeypatch.setenv("PAM_CD_FORM", "residual")  # few fits would pick the covariance form
     field = pam.box_field_2d(*cells)
     part = pam.make_partition(field.mesh, px, 1)
     cfg = pam.AdaptiveConfig(k_top=24, m_max=150, m_q=3, max_rounds=3, elastic=EN_2D,
@@ -430,3 +434,27 @@ def test_pipelined_few_fit_kernel_matches_lean(cuda, monkeypatch, cells, px):
         for x, y in zip(ra, rb):
             assert (x.centers, x.added) == (y.centers, y.added)
             assert abs(x.objective - y.objective) <= 1e-10 * abs(x.objective)
+
+
+def test_wide_gram_form_for_few_fits_matches_residual(cuda, monkeypatch):
+    """Few fits with a wide dictionary (M > 512): the host picks the covariance
+    form (gram.cu wide configurations, engine.cd_form); same dictionaries and
+    reports as the residual form, beta ~1e-12."""
+    field = pam.box_field_2d(32, 32)
+    part = pam.make_partition(field.mesh, 1, 1)  # 1,024 cells, per-cell dictionary
+    cfg = pam.AdaptiveConfig(k_top=24, m_max=150, m_q=3, max_rounds=3, elastic=EN_2D,
+                             offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
+    spec = pam.DictionarySpec(sigma=1.0 / 32)
+    from paper_2605_16564_b200 import engine as E
+    assert E.cd_form([1024], [1024 + 144]) == "gram"
+    monkeypatch.setenv("PAM_CD_FORM", "residual")
+    res, rr = pam.fit_parallel(field, part, cfg, spec)
+    monkeypatch.setenv("PAM_CD_FORM", "auto")
+    gram, rg = pam.fit_parallel(field, part, cfg, spec)
+    for a, b in zip(res.locals, gram.locals):
+        np.testing.assert_array_equal(a.dictionary.centers, b.dictionary.centers)
+        assert np.max(np.abs(a.beta - b.beta)) <= 1e-9 * max(1, np.abs(a.beta).max())
+    for ra, rb in zip(rr.rounds, rg.rounds):
+        for x, y in zip(ra, rb):
+            assert (x.centers, x.added) == (y.centers, y.added)
+            assert abs(x.objective - y.objective) <= 1e-9 * abs(x.objective)
