@@ -453,7 +453,10 @@ def run_c5(args):
     layers = args.c5_layers
     n_sub = 64 * 32 * layers
     n_eval = int(1e8 * layers / 32)
-    p = workloads.config5(M=args.m, n_sub=n_sub, n_eval=0)
+    if args.c5_gen == "device":  # pam_c5_generate_f64: same distributions, counter-based stream
+        p = workloads.config5_device(M=args.m, n_sub=n_sub)
+    else:
+        p = workloads.config5(M=args.m, n_sub=n_sub, n_eval=0)
     # 1e8 uniform points over the full 64x32x32 domain, restricted to the fitted slab
     p.eval_points = np.random.default_rng(50).random((n_eval, 3)) * np.array([64.0, 32.0, float(layers)])
     dev = nat.device()
@@ -541,6 +544,8 @@ def main():
     ap.add_argument("--config", default="C4", choices=["C4", "C5"])
     ap.add_argument("--m", type=int, default=256, help="C5: centres per subdomain")
     ap.add_argument("--c5-layers", type=int, default=4, help="C5: z-layers of the 64x32 box grid")
+    ap.add_argument("--c5-gen", default="host", choices=["host", "device"],
+                    help="C5 inputs: numpy generator (as the parity tests) or the on-device generator")
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)

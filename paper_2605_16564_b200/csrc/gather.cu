@@ -113,3 +113,116 @@ extern "C" int pam_row_normalize_f64(int64_t N, int64_t M, const double* in, int
   PAM_LAUNCH_CHECK("row_normalize_kernel");
   return PAM_OK;
 }
+
+// ---------------------------------------------------------------------------
+// On-device generator of BASELINE config 5 inputs: unit
+// boxes of a gx x gy x gz tiling (x fastest), n_pts uniform samples per box,
+// 1-4 planar interfaces through uniform points with uniform normals and
+// per-region levels 10^U[-3,3], and a jittered (lx, ly, lz) centre lattice
+// (offsets U(-1/4, 1/4) of the spacing, clamped to the box).  Same
+// distributions as workloads.config5 (host, numpy), different random stream:
+// counter-based SplitMix64 hashes of (seed, box, stream, index), so the data
+// are identical for any launch shape and deterministic.
+namespace pam {
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+// uniform double in [0, 1) from (seed, box, stream, index)
+__device__ __forceinline__ double u01(uint64_t seed, uint64_t box, uint32_t stream, uint64_t i) {
+  const uint64_t h = mix64(seed ^ mix64(box * 0x100000001B3ull + stream) ^ mix64(i + 0x632BE59BD9B4E019ull));
+  return static_cast<double>(h >> 11) * 0x1.0p-53;
+}
+
+struct C5Box {
+  int k;
+  double lo[3];
+  double nrm[4][3];
+  double thr[4][3];
+  double lev[16];
+};
+
+__device__ void c5_box(uint64_t seed, int64_t s, int gx, int gy, C5Box& b) {
+  b.lo[0] = static_cast<double>(s % gx);
+  b.lo[1] = static_cast<double>((s / gx) % gy);
+  b.lo[2] = static_cast<double>(s / (static_cast<int64_t>(gx) * gy));
+  b.k = 1 + min(3, static_cast<int>(u01(seed, s, 1, 0) * 4.0));
+  for (int p = 0; p < b.k; ++p) {
+    // uniform direction: normalised Gaussian triple (Box-Muller)
+    double v[3], nn = 0.0;
+    for (int c = 0; c < 3; ++c) {
+      const double u1 = 1.0 - u01(seed, s, 2, 6 * p + 2 * c), u2 = u01(seed, s, 2, 6 * p + 2 * c + 1);
+      v[c] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+      nn += v[c] * v[c];
+    }
+    nn = sqrt(nn);
+    for (int c = 0; c < 3; ++c) {
+      b.nrm[p][c] = v[c] / nn;
+      b.thr[p][c] = b.lo[c] + u01(seed, s, 3, 3 * p + c);
+    }
+  }
+  for (int r = 0; r < (1 << b.k); ++r) b.lev[r] = exp10(-3.0 + 6.0 * u01(seed, s, 4, r));
+}
+
+__global__ void c5_points_kernel(int64_t n_sub, int n_pts, int gx, int gy, uint64_t seed, double* pts,
+                                 double* vals) {
+  __shared__ C5Box b;
+  for (int64_t s = blockIdx.x; s < n_sub; s += gridDim.x) {
+    __syncthreads();
+    if (threadIdx.x == 0) c5_box(seed, s, gx, gy, b);
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_pts; i += blockDim.x) {
+      const int64_t row = s * n_pts + i;
+      double x[3];
+      for (int c = 0; c < 3; ++c) {
+        x[c] = b.lo[c] + u01(seed, s, 5, 3 * static_cast<uint64_t>(i) + c);
+        pts[row * 3 + c] = x[c];
+      }
+      int region = 0;
+      for (int p = 0; p < b.k; ++p) {
+        double side = 0.0;
+        for (int c = 0; c < 3; ++c) side += (x[c] - b.thr[p][c]) * b.nrm[p][c];
+        region |= (side > 0.0 ? 1 : 0) << p;
+      }
+      vals[row] = b.lev[region];
+    }
+  }
+}
+
+__global__ void c5_centres_kernel(int64_t n_sub, int lx, int ly, int lz, int gx, int gy, uint64_t seed,
+                                  double* cen) {
+  const int M = lx * ly * lz;
+  const double h[3] = {1.0 / lx, 1.0 / ly, 1.0 / lz};
+  const int64_t total = n_sub * M;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = e / M;
+    const int m = static_cast<int>(e % M);
+    const int li[3] = {m % lx, (m / lx) % ly, m / (lx * ly)};
+    const double lo[3] = {static_cast<double>(s % gx), static_cast<double>((s / gx) % gy),
+                          static_cast<double>(s / (static_cast<int64_t>(gx) * gy))};
+    for (int c = 0; c < 3; ++c) {
+      const double j = (u01(seed, s, 6, 3 * static_cast<uint64_t>(m) + c) - 0.5) * 0.5 * h[c];
+      const double v = lo[c] + (li[c] + 0.5) * h[c] + j;
+      cen[e * 3 + c] = fmin(fmax(v, lo[c]), lo[c] + 1.0);
+    }
+  }
+}
+
+}  // namespace pam
+
+extern "C" int pam_c5_generate_f64(int64_t n_sub, int32_t n_pts, int32_t lx, int32_t ly, int32_t lz,
+                                   int32_t gx, int32_t gy, uint64_t seed, double* points, double* values,
+                                   double* centres, void* stream) {
+  if (n_sub < 1 || n_pts < 1 || lx < 1 || ly < 1 || lz < 1 || gx < 1 || gy < 1) return PAM_ERR_ARG;
+  cudaStream_t st = as_stream(stream);
+  const int blocks = static_cast<int>(std::min<int64_t>(n_sub, 148 * 16));
+  c5_points_kernel<<<blocks, 256, 0, st>>>(n_sub, n_pts, gx, gy, seed, points, values);
+  PAM_LAUNCH_CHECK("c5_points_kernel");
+  c5_centres_kernel<<<148 * 8, 256, 0, st>>>(n_sub, lx, ly, lz, gx, gy, seed, centres);
+  PAM_LAUNCH_CHECK("c5_centres_kernel");
+  return PAM_OK;
+}

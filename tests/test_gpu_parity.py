@@ -458,3 +458,34 @@ def test_wide_gram_form_for_few_fits_matches_residual(cuda, monkeypatch):
         for x, y in zip(ra, rb):
             assert (x.centers, x.added) == (y.centers, y.added)
             assert abs(x.objective - y.objective) <= 1e-9 * abs(x.objective)
+
+
+def test_c5_device_generator(cuda):
+    """On-device config-5 inputs (pam_c5_generate_f64): deterministic, the
+    distributions of workloads.config5 (points in their half-open unit box,
+    levels in [1e-3, 1e3] with at most 16 per box, centres within a quarter
+    spacing of the lattice and inside the box), and they fit like the host
+    generator's data (oracle parity on two boxes)."""
+    p = workloads.config5_device(M=64, n_sub=64, n_pts=1000, seed=11)
+    q = workloads.config5_device(M=64, n_sub=64, n_pts=1000, seed=11)
+    np.testing.assert_array_equal(p.points, q.points)
+    np.testing.assert_array_equal(p.values, q.values)
+    np.testing.assert_array_equal(p.centres, q.centres)
+    pts = p.points.reshape(64, 1000, 3)
+    assert np.all(pts >= p.box_lo[:, None, :]) and np.all(pts < p.box_hi[:, None, :])
+    assert np.all(p.values >= 1e-3) and np.all(p.values <= 1e3)
+    assert max(len(np.unique(p.values[s * 1000:(s + 1) * 1000])) for s in range(64)) <= 16
+    assert np.mean(pts, axis=(0, 1)) == pytest.approx(np.mean(p.box_lo, axis=0) + 0.5, abs=0.01)
+    cen = p.centres.reshape(64, 64, 3)
+    m = np.arange(64)
+    lat = (np.stack([m % 4, (m // 4) % 4, m // 16], axis=1) + 0.5) * 0.25  # (4,4,4) lattice, x fastest
+    jit = cen - p.box_lo[:, None, :] - lat[None]
+    assert np.all(np.abs(jit) <= 0.25 * 0.25 + 1e-12)  # jitter within a quarter spacing
+    assert np.all(cen >= p.box_lo[:, None, :]) and np.all(cen <= p.box_hi[:, None, :])
+    res = pam.fit_subdomains(p)
+    c = p.config
+    for s in (0, 63):
+        a, b = p.row_off[s], p.row_off[s + 1]
+        W = O.shepard_features(p.points[a:b], p.centres[s * 64:(s + 1) * 64], p.widths[s * 64:(s + 1) * 64])
+        o = O.fit_log(p.values[a:b], W, c.elastic.lam1, c.elastic.lam2, c.elastic.tol, c.elastic.max_iters)
+        assert np.max(np.abs(res.beta[s] - o["beta"])) <= BETA_TOL * max(1, np.abs(o["beta"]).max())
