@@ -914,6 +914,346 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
 }
 
 // ----------------------------------------------------------------------------
+// Dual lean tile CD: two fits per warp, one per half-warp (<= 512 rows).
+//
+// The lean kernel at full C4 load (15 fits per SM) spends about a third of its
+// per-column time on issue contention between the ~4 fits per scheduler and
+// the rest on each fit's serial chain (occupancy probe).  Here a
+// warp carries two independent fits in its two 16-lane halves: one issued
+// instruction advances both, so the per-fit issue cost roughly halves, and the
+// per-column warp reduction is 4 butterfly levels instead of 5.  Lane h of a
+// half owns packed rows 32q + 2h + {0,1} (q = tile, R = 32 registers for 512
+// rows), so one 16-byte shared load per tile feeds two registers.  Both fits
+// walk a common column count Mx = max(M_a, M_b): columns past a fit's own M
+// and every column of a finished fit read the zero block and leave beta
+// unchanged (d = 0 exactly), so each half computes exactly what the one-fit
+// lean kernel computes.  Ring slots hold one column per half; each slot's
+// mbarrier takes one arrival per half (lanes 0 and 16 issue their half's bulk
+// copy, or a plain arrival for an empty column).  Pairs are consecutive
+// entries of the longest-first order, so paired fits have similar work.
+__device__ __forceinline__ double half_sum(double v) {
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double half_max(double v) {
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <int R, int STAGES, int WPC, int RUNS>
+__global__ void __launch_bounds__(WPC * 32, 1) cd_dual_kernel(const CdArgs a) {
+  constexpr int SLOTH = R * 16;  // doubles per half slot (one column of <= 16 R rows)
+  constexpr int PBLK = 144;      // doubles per warp: pb/pc/pinv[32] + pk/ioff/icode[32] (index half*16 + c)
+  static_assert(R % 2 == 0 && R <= 32 && STAGES <= 8, "dual lean tile CD envelope");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int half = lane >> 4;
+  const int hl = lane & 15;
+  const int hb = half * 16;  // this half's index base in the parameter blocks
+  double* const ring_all = reinterpret_cast<double*>(smem_raw);
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(ring_all + static_cast<size_t>(WPC) * STAGES * 2 * SLOTH) +
+                         warp * STAGES;
+  double* const pb = reinterpret_cast<double*>(reinterpret_cast<uint64_t*>(
+                         ring_all + static_cast<size_t>(WPC) * STAGES * 2 * SLOTH) + WPC * STAGES) +
+                     warp * PBLK;
+  double* const pc = pb + 32;
+  double* const pinv = pb + 64;
+  int* const pk = reinterpret_cast<int*>(pb + 96);
+  int* const ioff = pk + 32;
+  int* const icode = pk + 64;
+  double* const zero_blk = reinterpret_cast<double*>(reinterpret_cast<uint64_t*>(
+                               ring_all + static_cast<size_t>(WPC) * STAGES * 2 * SLOTH) + WPC * STAGES) +
+                           WPC * PBLK;
+  // slot st of this half: ring_h + st * (2 * SLOTH * 8) bytes
+  const uint32_t ring_h = smem_u32(ring_all + static_cast<size_t>(warp) * STAGES * 2 * SLOTH) + half * (SLOTH * 8);
+  const uint32_t bar_s = smem_u32(bars);
+  const uint32_t zero_s = smem_u32(zero_blk) + 16u * hl;
+  constexpr uint32_t SLOT_B = 2u * SLOTH * 8u;
+
+  for (int i = threadIdx.x; i < SLOTH; i += WPC * 32) zero_blk[i] = 0.0;
+  if (lane == 0) {
+    for (int i = 0; i < STAGES; ++i) mbar_init(&bars[i], 2);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  int st = 0;
+  uint32_t ph = 0;
+  int ist = 0;
+  const int64_t P = (a.S + 1) / 2;  // fit pairs
+  unsigned item = warp * gridDim.x + blockIdx.x;
+  const unsigned total_warps = gridDim.x * WPC;
+
+  while (item < P) {
+    const int64_t idx = 2 * static_cast<int64_t>(item) + half;
+    int64_t s = -1;
+    if (idx < a.S) {
+      s = a.order ? a.order[idx] : idx;
+      if (a.active != nullptr && a.active[s] == 0) s = -1;
+    }
+    const bool hvalid = s >= 0;
+    const int64_t sx = hvalid ? s : 0;
+    const int64_t r0 = a.row_off[sx];
+    const int N = hvalid ? static_cast<int>(a.row_off[sx + 1] - r0) : 0;
+    const int M = hvalid ? a.m_cur[sx] : 0;
+    const int64_t doff = a.dict_off[sx];
+    const double* Ws = a.W + a.w_off[sx];
+    const int64_t* colo = a.col_off + doff;
+    const unsigned long long* tmk = a.tile_mask + doff;
+    double* betas = a.beta + doff;
+    double* colsq = a.col_sq + doff;
+    const double lam1 = a.lam1[sx], lam2 = a.lam2[sx], tol = a.tol[sx];
+    const int mi = hvalid ? a.max_iters[sx] : 0;
+    const int Mo = __shfl_xor_sync(0xffffffffu, M, 16);
+    const int Mx = M > Mo ? M : Mo;
+    const int mio = __shfl_xor_sync(0xffffffffu, mi, 16);
+    const int mix = mi > mio ? mi : mio;
+
+    double r[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int p = 32 * (k >> 1) + 2 * hl + (k & 1);
+      const int row = a.perm ? (p < N ? a.perm[r0 + p] : 0) : p;
+      r[k] = (p < N) ? a.y[r0 + row] : 0.0;
+    }
+
+    // ---- issue side: column stream = [prologue Mx] + mix * Mx (both halves in step)
+    const int64_t total = static_cast<int64_t>(Mx) * (1 + mix);
+    int64_t issued = 0;
+    int next_col = 0;
+    bool live = hvalid;  // this half still streams real columns (cleared on convergence)
+    int pf_off = 0, pf_code = 0;
+    auto fetch_issue = [&](int cb) {
+      const int c = cb + hl;
+      pf_off = (c < M) ? static_cast<int>(colo[c]) : 0;
+      pf_code = (c < M) ? tile_code(tmk[c]) : 0;
+    };
+    fetch_issue(0);
+    auto issue_one = [&](double dep) {
+      const int c = next_col & 15;
+      if (c == 0) {
+        __syncwarp();
+        ioff[hb + hl] = pf_off;
+        icode[hb + hl] = pf_code;
+        __syncwarp();
+        fetch_issue(next_col + 16 < Mx ? next_col + 16 : 0);
+      }
+      if (hl == 0) {
+        const int code = live ? icode[hb + c] : 0;
+        const uint32_t bytes = static_cast<uint32_t>(code_tiles(code)) * 256u;
+        const uint32_t bar = bar_s + ist * 8;
+        if (bytes) {
+          mbar_expect_s(bar, bytes);
+          bulk_g2s_dep(ring_h + ist * SLOT_B, Ws + ioff[hb + c], bytes, bar, dep);
+        } else {
+          mbar_arrive_s(bar);
+        }
+      }
+      if (++ist == STAGES) ist = 0;
+      ++issued;
+      if (++next_col == Mx) next_col = 0;
+    };
+    for (int q = 0; q < STAGES && issued < total; ++q) issue_one(0.0);
+
+    // ---- consumer side
+    int64_t consumed = 0;
+    bool ready = false;
+    double w[R];
+    auto load_w = [&](int code) {
+      if (!ready) mbar_wait_s(bar_s + st * 8, ph);
+      const int a0 = code & 0xff, la = (code >> 8) & 0xff;
+      const int b0 = (code >> 16) & 0xff, lb = code >> 24;
+      const uint32_t cA = ring_h + st * SLOT_B + 16u * hl - 256u * a0;
+      const uint32_t cB = ring_h + st * SLOT_B + 16u * hl + 256u * (la - b0);
+#pragma unroll
+      for (int q = 0; q < R / 2; ++q) {
+        const bool inA = static_cast<unsigned>(q - a0) < static_cast<unsigned>(la);
+        uint32_t ad;
+        if (RUNS == 1) {
+          ad = inA ? cA : zero_s;
+        } else {
+          const bool inB = static_cast<unsigned>(q - b0) < static_cast<unsigned>(lb);
+          ad = inA ? cA : (inB ? cB : zero_s);
+        }
+        lds_v2(ad + 256u * q, w[2 * q], w[2 * q + 1]);
+      }
+    };
+    auto advance = [&](double dep) {
+      if (issued < total) issue_one(dep);
+      if (++st == STAGES) {
+        st = 0;
+        ph ^= 1u;
+      }
+      ++consumed;
+      ready = (consumed < issued) && mbar_test_s(bar_s + st * 8, ph);
+    };
+
+    // prologue: col_sq (elastic_net.py:85) and r = y - W beta0 (elastic_net.py:94)
+    for (int cb = 0; cb < Mx; cb += 16) {
+      const int nc = min(16, Mx - cb);
+      int cl = 0;
+      double bl0 = 0.0, csl = 0.0;
+      if (cb + hl < M) {
+        cl = tile_code(tmk[cb + hl]);
+        bl0 = betas[cb + hl];
+      }
+      for (int t = 0; t < nc; ++t) {
+        load_w(__shfl_sync(0xffffffffu, cl, t, 16));
+        double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          if (k & 1) p1 = fma(w[k], w[k], p1);
+          else p0 = fma(w[k], w[k], p0);
+        }
+        const double pp = p0 + p1;
+        advance(pp);
+        const double p = half_sum(pp);
+        if (hl == t) csl = p;
+        const double b0 = __shfl_sync(0xffffffffu, bl0, t, 16);
+        if (__any_sync(0xffffffffu, b0 != 0.0)) {
+#pragma unroll
+          for (int k = 0; k < R; ++k) r[k] = fma(-b0, w[k], r[k]);
+        }
+      }
+      if (cb + hl < M) colsq[cb + hl] = csl;
+    }
+
+    // sweeps (elastic_net.py:137-161)
+    const bool one_chunk = Mx <= 16;
+    double nb_l = 0.0, ncs_l = 0.0;
+    int nk_l = 0;
+    auto fetch_params = [&](int cb) {
+      const int c = cb + hl;
+      nb_l = (c < M) ? betas[c] : 0.0;
+      ncs_l = (c < M) ? colsq[c] : 0.0;
+      nk_l = (c < M) ? tile_code(tmk[c]) : 0;
+    };
+    fetch_params(0);
+    int sweeps_done = 0, conv = 0;
+    double obj = 0.0;
+    for (int sw = 0; sw < mix; ++sw) {
+      const bool act = hvalid && !conv && sw < mi;
+      if (!__any_sync(0xffffffffu, act)) break;
+      double max_delta = 0.0, acc_l1 = 0.0, acc_l2 = 0.0, acc_max = 0.0;
+      for (int cb = 0; cb < Mx; cb += 16) {
+        const int nc = min(16, Mx - cb);
+        __syncwarp();
+        if (sw == 0 || !one_chunk) {
+          pb[hb + hl] = nb_l;
+          pc[hb + hl] = ncs_l;
+          const double dnv = __dadd_rn(ncs_l, lam2);
+          pinv[hb + hl] = dnv > 0.0 ? __ddiv_rn(1.0, dnv) : 0.0;
+          pk[hb + hl] = nk_l;
+          if (!one_chunk) fetch_params(cb + 16 < Mx ? cb + 16 : 0);
+        }
+        __syncwarp();
+        for (int t = 0; t < nc; ++t) {
+          load_w(act ? pk[hb + t] : 0);  // a finished half reads zeros
+          double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            if ((k & 3) == 0) d0 = fma(w[k], r[k], d0);
+            else if ((k & 3) == 1) d1 = fma(w[k], r[k], d1);
+            else if ((k & 3) == 2) d2 = fma(w[k], r[k], d2);
+            else d3 = fma(w[k], r[k], d3);
+          }
+          const double part = (d0 + d1) + (d2 + d3);
+          advance(part);
+          const double b_old = pb[hb + t];
+          const double cs = pc[hb + t];
+          const double inv = pinv[hb + t];
+          const double cb_old = __dmul_rn(cs, b_old);
+          const double dn = __dadd_rn(cs, lam2);
+          const double dot = half_sum(part);
+          const double z = __dadd_rn(cb_old, dot);
+          const double np_ = __dsub_rn(z, lam1), nn_ = __dadd_rn(z, lam1);
+          const double qp = __dmul_rn(np_, inv), qn = __dmul_rn(nn_, inv);
+          const double bp = fma(fma(-qp, dn, np_), inv, qp);
+          const double bn = fma(fma(-qn, dn, nn_), inv, qn);
+          double b_new = np_ > 0.0 ? bp : (nn_ < 0.0 ? bn : 0.0);
+          if (!act) b_new = b_old;
+          const double d = __dsub_rn(b_new, b_old);
+#pragma unroll
+          for (int k = 0; k < R; ++k) r[k] = fma(-d, w[k], r[k]);
+          if (hl == 0) pb[hb + t] = b_new;
+          const double ad = fabs(d);
+          max_delta = ad > max_delta ? ad : max_delta;
+        }
+        __syncwarp();
+        if (act && hl < nc && cb + hl < M) {
+          const double bl = pb[hb + hl];
+          betas[cb + hl] = bl;
+          const double ab = fabs(bl);
+          acc_l1 += ab;
+          acc_l2 = fma(bl, bl, acc_l2);
+          acc_max = fmax(acc_max, ab);
+        }
+      }
+      double rss0 = 0.0, rss1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        if (k & 1) rss1 = fma(r[k], r[k], rss1);
+        else rss0 = fma(r[k], r[k], rss0);
+      }
+      const double rss = half_sum(rss0 + rss1);
+      const double l1 = half_sum(acc_l1);
+      const double l2 = half_sum(acc_l2);
+      const double mabs = half_max(acc_max);
+      if (act) {
+        obj = __dadd_rn(__dadd_rn(__dmul_rn(0.5, rss), __dmul_rn(lam1, l1)),
+                        __dmul_rn(__dmul_rn(0.5, lam2), l2));
+        if (a.hist != nullptr && hl == 0) a.hist[a.hist_off[s] + sw] = obj;
+        sweeps_done = sw + 1;
+        if (max_delta <= __dmul_rn(tol, fmax(mabs, 1.0))) {
+          conv = 1;
+          live = false;  // later stream positions of this half carry no data
+        }
+      }
+    }
+    const bool zero_it = hvalid && mi == 0;
+    if (__any_sync(0xffffffffu, zero_it)) {
+      // objective at the given beta (after the Gram-form sweeps, gram.cu);
+      // both halves run the shuffles, only a half with max_iters == 0 keeps it
+      double rss = 0.0, l1 = 0.0, l2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < R; ++k) rss = fma(r[k], r[k], rss);
+      rss = half_sum(rss);
+      for (int j = hl; j < M; j += 16) {
+        const double b = betas[j];
+        l1 += fabs(b);
+        l2 = fma(b, b, l2);
+      }
+      l1 = half_sum(l1);
+      l2 = half_sum(l2);
+      if (zero_it)
+        obj = __dadd_rn(__dadd_rn(__dmul_rn(0.5, rss), __dmul_rn(lam1, l1)),
+                        __dmul_rn(__dmul_rn(0.5, lam2), l2));
+    }
+    // drain the prefetched columns of the sweep that will not run
+    while (consumed < issued) {
+      mbar_wait_s(bar_s + st * 8, ph);
+      if (++st == STAGES) {
+        st = 0;
+        ph ^= 1u;
+      }
+      ++consumed;
+    }
+    __syncwarp();
+    if (hvalid && hl == 0) {
+      a.sweeps[s] = sweeps_done;
+      a.converged[s] = conv;
+      a.objective[s] = obj;
+    }
+    unsigned nxt = 0;
+    if (lane == 0) nxt = atomicAdd(&g_cd_queue, 1u) + total_warps;
+    item = __shfl_sync(0xffffffffu, nxt, 0);
+  }
+}
+
+// ----------------------------------------------------------------------------
 // Column-pair tile CD for batches of few fits (<= a few per SM: BASELINE
 // configs 2-3, 64-256 fits of 1,024 rows).  With one or two fits per SM a
 // fit's per-column dependency chain (dot -> 5-level reduction -> soft
@@ -1247,6 +1587,43 @@ int launch_cd_tile_r(const CdArgs& a, cudaStream_t stream) {
   return PAM_OK;
 }
 
+template <int R, int STAGES, int WPC, int RUNS>
+int launch_cd_dual(const CdArgs& a, cudaStream_t stream) {
+  constexpr int SLOTH = R * 16;
+  const size_t smem = static_cast<size_t>(WPC) * STAGES * 2 * SLOTH * sizeof(double) +
+                      static_cast<size_t>(WPC) * STAGES * sizeof(uint64_t) +
+                      static_cast<size_t>(WPC) * 144 * sizeof(double) + SLOTH * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    PAM_CUDA_CHECK(cudaFuncSetAttribute(cd_dual_kernel<R, STAGES, WPC, RUNS>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  int dev = 0, sms = 148;
+  PAM_CUDA_CHECK(cudaGetDevice(&dev));
+  PAM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  void* qaddr = nullptr;
+  PAM_CUDA_CHECK(cudaGetSymbolAddress(&qaddr, g_cd_queue));
+  PAM_CUDA_CHECK(cudaMemsetAsync(qaddr, 0, sizeof(unsigned), stream));
+  const int64_t pairs = (a.S + 1) / 2;
+  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(sms, pairs));
+  cd_dual_kernel<R, STAGES, WPC, RUNS><<<(unsigned)ctas, WPC * 32, smem, stream>>>(a);
+  PAM_LAUNCH_CHECK("cd_dual_kernel");
+  return PAM_OK;
+}
+
+// Two fits per warp for 257-512 rows when the batch fills >= 8 fits per SM
+// (C4: 15); below that the one-fit warps' shorter chains win.  PAM_CD_DUAL:
+// 1 forces the dual kernel, 0 disables it.
+inline bool cd_use_dual(int64_t S) {
+  const char* env = getenv("PAM_CD_DUAL");
+  if (env) return atoi(env) == 1;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return S >= 8LL * sms;
+}
+
 template <int R, int STAGES, int WPC, int G, bool TILES = false, bool KEEPW = true, bool LDGSTS = false>
 int launch_cd(const CdArgs& a, cudaStream_t stream) {
   constexpr int NGROUPS = WPC / G;
@@ -1375,6 +1752,12 @@ int cd_dispatch_tiles(const CdArgs& a, int max_rows, cudaStream_t stream) {
     if (max_rows <= 128) return launch_cd_tile<4, 4, 16>(a, stream);
     if (max_rows <= 256) return launch_cd_tile<8, 4, 16>(a, stream);
     if (max_rows <= 512) {
+      if (max_rows > 256 && cd_use_dual(a.S)) {
+        const char* de = getenv("PAM_CD_DUAL_STAGES");  // ring-depth probe
+        if (de && atoi(de) == 2) return launch_cd_dual<32, 2, 8, 1>(a, stream);
+        if (tile_runs() == 1) return launch_cd_dual<32, 3, 8, 1>(a, stream);
+        return launch_cd_dual<32, 3, 8, 2>(a, stream);
+      }
       const char* se = getenv("PAM_CD_STAGES");
       if (se && atoi(se) == 4) return launch_cd_tile<16, 4, 12>(a, stream);  // deeper ring, 12 warps
       return launch_cd_tile<16, 3, 16>(a, stream);

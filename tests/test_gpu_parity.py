@@ -489,3 +489,32 @@ def test_c5_device_generator(cuda):
         W = O.shepard_features(p.points[a:b], p.centres[s * 64:(s + 1) * 64], p.widths[s * 64:(s + 1) * 64])
         o = O.fit_log(p.values[a:b], W, c.elastic.lam1, c.elastic.lam2, c.elastic.tol, c.elastic.max_iters)
         assert np.max(np.abs(res.beta[s] - o["beta"])) <= BETA_TOL * max(1, np.abs(o["beta"]).max())
+
+
+@pytest.mark.parametrize("cells,parts,tol", [((60, 60), (3, 3), 1e-6), ((48, 36), (2, 2), 1e-6),
+                                             ((60, 60), (3, 3), 1e-3), ((50, 50), (5, 1), 1e-4)])
+def test_dual_fit_kernel_matches_lean(cuda, monkeypatch, cells, parts, tol):
+    """Two fits per warp (cd.cu cd_dual_kernel, one fit per half-warp, 257-512
+    rows) against the one-fit-per-warp lean kernel: odd fit counts (a lone
+    half), ragged dictionaries after enrichment (padded columns), fits that
+    converge at different sweeps (a finished half idles on zero columns).
+    Same dictionaries, sweeps within one, beta and objectives ~1e-12."""
+    monkeypatch.setenv("PAM_CD_FORM", "residual")
+    monkeypatch.setenv("PAM_CD_PIPE", "0")
+    field = pam.box_field_2d(*cells)
+    part = pam.make_partition(field.mesh, *parts)
+    en = pam.ElasticNetConfig(lam1=4.59e-4, lam2=1e-4, tol=tol, max_iters=1500)
+    cfg = pam.AdaptiveConfig(k_top=40, m_max=240, m_q=3, max_rounds=3, elastic=en,
+                             offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
+    spec = pam.DictionarySpec(sigma=0.5 / cells[0])
+    monkeypatch.setenv("PAM_CD_DUAL", "0")
+    lean, rl = pam.fit_parallel(field, part, cfg, spec)
+    monkeypatch.setenv("PAM_CD_DUAL", "1")
+    dual, rd = pam.fit_parallel(field, part, cfg, spec)
+    for a, b in zip(lean.locals, dual.locals):
+        np.testing.assert_array_equal(a.dictionary.centers, b.dictionary.centers)
+        assert np.max(np.abs(a.beta - b.beta)) <= 1e-10 * max(1, np.abs(a.beta).max())
+    for ra, rb in zip(rl.rounds, rd.rounds):
+        for x, y in zip(ra, rb):
+            assert (x.centers, x.added) == (y.centers, y.added)
+            assert abs(x.objective - y.objective) <= 1e-10 * abs(x.objective)
