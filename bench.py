@@ -420,6 +420,9 @@ def cd_kernel_name() -> str:
     lean = os.environ.get("PAM_CD_LEAN", "1")
     if runs == "0" or lean == "0":
         return "cd_kernel (generic tile stream, TMA)"
+    if os.environ.get("PAM_CD_DUAL", "") != "0":
+        # C4: 2,244 fits of 500 rows >= 8 fits per SM (cd.cu cd_use_dual)
+        return "cd_dual_kernel (lean tile stream, two fits per warp, TMA)"
     return "cd_tile_kernel (lean single-column tile stream, TMA)"
 
 
