@@ -603,11 +603,14 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
       const int total = M * (1 + max_iters);
       int issued = 0;
       int next_col = 0;
-      int pf_off = 0, pf_code = 0;  // issue parameters of the next chunk (lane = column)
+      // issue parameters of the next chunk (lane = column); the mask is decoded
+      // at publish time so the global load's latency stays off the column loop
+      int pf_off = 0;
+      unsigned long long pf_mk = 0ull;
       auto fetch_issue = [&](int cb) {
         const int c = cb + lane;
         pf_off = (c < M) ? static_cast<int>(colo[c]) : 0;
-        pf_code = (c < M) ? tile_code(tmk[c]) : 0;
+        pf_mk = (c < M) ? tmk[c] : 0ull;
       };
       fetch_issue(0);
       // dep: a value computed from this warp's loads of the slot being refilled,
@@ -617,7 +620,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
         if (c == 0) {
           __syncwarp();
           ioff[lane] = pf_off;
-          icode[lane] = pf_code;
+          icode[lane] = tile_code(pf_mk);
           __syncwarp();
           fetch_issue(next_col + 32 < M ? next_col + 32 : 0);
         }
@@ -764,12 +767,12 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
       // sweeps (elastic_net.py:137-161); chunk parameters prefetched one chunk ahead
       const bool one_chunk = M <= 32;
       double nb_l = 0.0, ncs_l = 0.0;
-      int nk_l = 0;
+      unsigned long long nk_mk = 0ull;  // decoded at publish time
       auto fetch_params = [&](int cb) {
         const int c = cb + lane;
         nb_l = (c < M) ? betas[c] : 0.0;
         ncs_l = (c < M) ? colsq[c] : 0.0;
-        nk_l = (c < M) ? tile_code(tmk[c]) : 0;
+        nk_mk = (c < M) ? tmk[c] : 0ull;
       };
       fetch_params(0);
       int sweeps_done = 0, conv = 0;
@@ -787,7 +790,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
             pc[lane] = ncs_l;
             const double dnv = __dadd_rn(ncs_l, lam2);
             pinv[lane] = dnv > 0.0 ? __ddiv_rn(1.0, dnv) : 0.0;
-            pk[lane] = nk_l;
+            pk[lane] = tile_code(nk_mk);
             if (!one_chunk) fetch_params(cb + 32 < M ? cb + 32 : 0);
           }
           __syncwarp();
@@ -1025,11 +1028,14 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_dual_kernel(const CdArgs a) {
     int64_t issued = 0;
     int next_col = 0;
     bool live = hvalid;  // this half still streams real columns (cleared on convergence)
-    int pf_off = 0, pf_code = 0;
+    // next chunk's issue parameters; the mask is decoded at publish time, one
+    // chunk later, so the global load's latency stays off the column loop
+    int pf_off = 0;
+    unsigned long long pf_mk = 0ull;
     auto fetch_issue = [&](int cb) {
       const int c = cb + hl;
       pf_off = (c < M) ? static_cast<int>(colo[c]) : 0;
-      pf_code = (c < M) ? tile_code(tmk[c]) : 0;
+      pf_mk = (c < M) ? tmk[c] : 0ull;
     };
     fetch_issue(0);
     auto issue_one = [&](double dep) {
@@ -1037,7 +1043,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_dual_kernel(const CdArgs a) {
       if (c == 0) {
         __syncwarp();
         ioff[hb + hl] = pf_off;
-        icode[hb + hl] = pf_code;
+        icode[hb + hl] = tile_code(pf_mk);
         __syncwarp();
         fetch_issue(next_col + 16 < Mx ? next_col + 16 : 0);
       }
@@ -1124,12 +1130,12 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_dual_kernel(const CdArgs a) {
     // sweeps (elastic_net.py:137-161)
     const bool one_chunk = Mx <= 16;
     double nb_l = 0.0, ncs_l = 0.0;
-    int nk_l = 0;
+    unsigned long long nk_mk = 0ull;  // decoded at publish time (see fetch_issue)
     auto fetch_params = [&](int cb) {
       const int c = cb + hl;
       nb_l = (c < M) ? betas[c] : 0.0;
       ncs_l = (c < M) ? colsq[c] : 0.0;
-      nk_l = (c < M) ? tile_code(tmk[c]) : 0;
+      nk_mk = (c < M) ? tmk[c] : 0ull;
     };
     fetch_params(0);
     int sweeps_done = 0, conv = 0;
@@ -1146,7 +1152,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_dual_kernel(const CdArgs a) {
           pc[hb + hl] = ncs_l;
           const double dnv = __dadd_rn(ncs_l, lam2);
           pinv[hb + hl] = dnv > 0.0 ? __ddiv_rn(1.0, dnv) : 0.0;
-          pk[hb + hl] = nk_l;
+          pk[hb + hl] = tile_code(nk_mk);
           if (!one_chunk) fetch_params(cb + 16 < Mx ? cb + 16 : 0);
         }
         __syncwarp();
