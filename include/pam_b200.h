@@ -163,7 +163,9 @@ int pam_cd_ex_f64(int64_t S, const int64_t* order, const int64_t* row_off, doubl
  * PAM_TILE_RUNS (default 1) contiguous runs of tiles (holes stored as their
  * exact small values).  pam_cd_tiles_f64 is pam_cd_f64 over that layout: one
  * cp.async.bulk of popcount(mask)*256 bytes per column; y is read through
- * perm. */
+ * perm.  Batches of 257-512-row fits with >= 8 fits per SM run two fits per
+ * warp (one per half-warp; PAM_CD_DUAL=0/1 overrides); results are the same
+ * either way up to dot-product rounding. */
 int pam_assemble_tiles_f64(int dim, int64_t S, const int64_t* row_off, const double* pts,
                            const int32_t* perm, const int64_t* dict_off, const int32_t* m_cur,
                            const double* centres, const double* widths, const int64_t* w_off,

@@ -21,7 +21,8 @@
 // pipeline bubble between sweeps.  Warps pull subdomains from a dynamic queue
 // (longest first, host-ordered) so the ragged batch stays balanced.  Each
 // sweep reads N*M*8 bytes: the kernel is HBM-bandwidth bound (SURVEY §8d,
-// K2b), ~2 FMA per 8 bytes.
+// K2b), ~2 FMA per 8 bytes.  For many fits of 257-512 rows (C4) the dual
+// kernel puts two fits in one warp, one per 16-lane half (cd_dual_kernel).
 #include "pam_common.cuh"
 
 #include <stdlib.h>
