@@ -223,6 +223,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2605_16564_b200 as pam
     from paper_2605_16564_b200 import _native as nat
+    from paper_2605_16564_b200 import engine as E
     from paper_2605_16564_b200 import workloads
     from paper_2605_16564_b200.partition import stage_field
 
@@ -365,6 +366,8 @@ def run_ours(args):
             "subdomains_per_gpu": n_sub, "eval_points_per_gpu": P,
             "l2": "inputs larger than L2 (design matrices ~10 GB per round)",
             "parallelism": f"replica-per-gpu x{world}",
+            "tile_tau": E.tile_tau(),
+            "cd_kernel": cd_kernel_name(),
         },
         "evals": {"value": world * P * args.steps / eval_s, "unit": "points/s",
                   "ms_per_step": eval_s / args.steps * 1e3},
@@ -375,7 +378,7 @@ def run_ours(args):
                      "avg_launch_s": cd_s / max(cd_launches, 1),
                      "fp64_gflops": cd_flops / cd_s / 1e9 if cd_s > 0 else 0.0,
                      "dense_equivalent_bytes_per_launch": cd_dense / max(cd_launches, 1),
-                     "tile_tau": __import__("paper_2605_16564_b200.engine", fromlist=["x"]).tile_tau(),
+                     "tile_tau": E.tile_tau(),
                      "step_share": cd_s / elapsed if elapsed else None},
         "eval_roofline": {"kernel": "eval_kernel (locate + owner sort + one-pass Shepard sum, table-driven FP64 exp)",
                           "bound": "fp64", "unit": "GFLOP/s",
@@ -413,16 +416,17 @@ def run_ours(args):
 
 
 def cd_kernel_name() -> str:
-    """The CD kernel the tile path dispatches to under the current environment (cd.cu)."""
-    if os.environ.get("PAM_TILE_TAU") == "0":
+    """The CD kernel the C4 batch dispatches to under the current engine options (cd.cu)."""
+    from paper_2605_16564_b200 import engine as E
+
+    o = E.OPTIONS
+    if o.tile_tau == 0:
         return "cd_kernel (dense column stream, TMA)"
-    runs = os.environ.get("PAM_TILE_RUNS", "1")
-    lean = os.environ.get("PAM_CD_LEAN", "1")
-    if runs == "0" or lean == "0":
-        return "cd_kernel (generic tile stream, TMA)"
-    if os.environ.get("PAM_CD_DUAL", "") != "0":
-        # C4: 2,244 fits of 500 rows >= 8 fits per SM (cd.cu cd_use_dual)
+    if o.cd_kernel in ("auto", "dual"):
+        # C4: 2,244 fits of 500 rows >= 8 fits per SM (cd.cu cd_dispatch_tiles)
         return "cd_dual_kernel (lean tile stream, two fits per warp, TMA)"
+    if o.cd_kernel == "pair":
+        return "cd_pipe_kernel (column pairs, TMA)"
     return "cd_tile_kernel (lean single-column tile stream, TMA)"
 
 
@@ -557,7 +561,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per CD launch from an ncu --set full capture (profiles/)")
+    ap.add_argument("--tile-tau", type=float, default=None, help="CD tile-drop threshold (0 = dense stream)")
+    ap.add_argument("--cd-kernel", default=None, choices=["auto", "lean", "dual", "pair"])
     args = ap.parse_args()
+    from paper_2605_16564_b200 import engine as E
+
+    if args.tile_tau is not None:
+        E.set_options(tile_tau=args.tile_tau)
+    if args.cd_kernel is not None:
+        E.set_options(cd_kernel=args.cd_kernel)
     if args.impl == "reference":
         return run_reference(args)
     if args.config == "C5":

@@ -32,12 +32,12 @@
  *                   the packed W buffer; column-major with leading dimension
  *                   ld[s] (int32, multiple of 16): W_s[i, j] = W[w_off+j*ld+i].
  *
- * Concurrency: the batched CD kernels (pam_cd_*_f64) balance subdomains
- * with a per-library device work counter, so CD calls must not run
- * concurrently on two streams of one device (the reference's own threading
- * model is one fit loop per process, partition.py:185-198).  The evaluation
- * entry points keep no global state (pam_eval_f64's tile queue lives in the
- * caller's workspace) and may overlap.
+ * Concurrency: no entry point keeps mutable global state.  The batched CD and
+ * evaluation kernels balance their work with a counter in the CALLER's
+ * device workspace (`work`), so calls on different streams (or different
+ * devices of one process) are independent as long as they use distinct
+ * workspaces.  Kernel attributes are set per call, so one process may drive
+ * several GPUs.  The host seams serialise per device on an internal arena.
  *
  * Citations are relative to the reference package root pkg/src/fieldfit/.
  */
@@ -61,12 +61,23 @@ extern "C" {
 #define PAM_ERR_NONFINITE 7    /* non-finite design/target (elastic_net.py:81-82)  */
 
 /* Version / capability probe: returns PAM_ABI_VERSION. */
-#define PAM_ABI_VERSION 1
+#define PAM_ABI_VERSION 2
 int pam_abi_version(void);
 /* Last CUDA error string recorded by the library (host memory, static). */
 const char* pam_last_error(void);
-/* Largest subdomain sample count the CD kernel accepts (rows per subdomain). */
+/* Largest subdomain sample count the CD kernels accept (rows per subdomain):
+ * the reference has no limit; fits above 8192 rows run the CTA-per-fit
+ * kernel with the residual in the workspace. */
 int64_t pam_cd_max_rows(void);
+
+/* CD kernel selection for pam_cd_tiles_f64 (`kernel`).  AUTO picks by batch
+ * shape (see pam_cd_tiles_f64); the others force one implementation (tests
+ * and A/B measurement).  Every choice computes the same CD up to the
+ * rounding of the length-N dot products. */
+#define PAM_CD_AUTO 0 /* by shape                                               */
+#define PAM_CD_LEAN 1 /* one fit per warp                                       */
+#define PAM_CD_DUAL 2 /* two fits per warp (257-512 rows)                       */
+#define PAM_CD_PAIR 3 /* column pairs, few fits per SM (33-1024 rows)           */
 
 /* err[0] = 0 (no error), err[1] = INT64_MAX. Device pointer. */
 int pam_err_reset(int64_t* err, void* stream);
@@ -130,14 +141,19 @@ int pam_c5_generate_f64(int64_t n_sub, int32_t n_pts, int32_t lx, int32_t ly, in
  * beta (packed like centres, dict_off) is the warm start on entry and the
  * solution on exit.  Outputs per subdomain: sweeps, converged, objective
  * (= history[sweeps-1]).  hist/hist_off may be NULL; otherwise the per-sweep
- * objective of subdomain s is written to hist[hist_off[s] + sweep]. */
+ * objective of subdomain s is written to hist[hist_off[s] + sweep].
+ * `work`: device workspace of pam_cd_workspace_bytes(S, sum N_s, max_rows)
+ * bytes (work counter; residual scratch for fits above 8192 rows).  Fits of
+ * up to 8192 rows keep the residual in registers (one warp, or a group of
+ * 4-8 warps when there are fewer than 4 fits per SM). */
+int64_t pam_cd_workspace_bytes(int64_t S, int64_t total_rows, int32_t max_rows);
 int pam_cd_f64(int64_t S, const int64_t* order, const int64_t* row_off, const double* y,
                const int64_t* dict_off, const int32_t* m_cur, const int64_t* w_off,
                const int32_t* ld, const double* W, const double* lam1, const double* lam2,
                const double* tol, const int32_t* max_iters, const int32_t* active,
                int32_t max_rows, double* beta, double* col_sq, int32_t* sweeps,
                int32_t* converged, double* objective, double* hist, const int64_t* hist_off,
-               void* stream);
+               void* work, void* stream);
 /* `order` (nullable): processing order of the S subdomains (longest first
  * balances the ragged batch); results do not depend on it.
  * pam_cd_ex_f64 adds `flags`: 1 = col_sq given (not recomputed), 2 = y holds
@@ -149,7 +165,7 @@ int pam_cd_ex_f64(int64_t S, const int64_t* order, const int64_t* row_off, doubl
                   const double* tol, const int32_t* max_iters, const int32_t* active,
                   int32_t max_rows, double* beta, double* col_sq, int32_t* sweeps,
                   int32_t* converged, double* objective, double* hist, const int64_t* hist_off,
-                  int flags, void* stream);
+                  int flags, void* work, void* stream);
 
 /* ---- K1t + K2b-tiles: tile-packed design matrices and their CD ------------
  * Same W as pam_assemble_f64 (mode 0) but stored for the CD stream as
@@ -159,13 +175,15 @@ int pam_cd_ex_f64(int64_t S, const int64_t* order, const int64_t* row_off, doubl
  * col_off[slot] = column offset (doubles) inside the subdomain's packed block
  * at W + w_off[s]; packed_total[s] = doubles stored.  rowmax/rowsum are
  * per-row scratch (sum N_s doubles each); total_slots = size of the slot
- * arrays.  Requires N_s <= 2048.  Each column's mask is closed to at most
- * PAM_TILE_RUNS (default 1) contiguous runs of tiles (holes stored as their
- * exact small values).  pam_cd_tiles_f64 is pam_cd_f64 over that layout: one
- * cp.async.bulk of popcount(mask)*256 bytes per column; y is read through
- * perm.  Batches of 257-512-row fits with >= 8 fits per SM run two fits per
- * warp (one per half-warp; PAM_CD_DUAL=0/1 overrides); results are the same
- * either way up to dot-product rounding. */
+ * arrays.  Requires N_s <= 1024.  Each column's mask is closed to ONE
+ * contiguous run of tiles (holes stored as their exact small values).
+ * pam_cd_tiles_f64 is pam_cd_f64 over that layout: one cp.async.bulk of
+ * popcount(mask)*256 bytes per column; y is read through perm; max_m = the
+ * largest m_cur of the batch (host-known; sizes the few-fit kernel's
+ * staging).  kernel = PAM_CD_AUTO: 257-1024-row fits with <= 3 fits per SM
+ * run the column-pair kernel, 257-512-row fits with >= 8 fits per SM two
+ * fits per warp, everything else one fit per warp; results are the same
+ * either way up to dot-product rounding.  `work` as for pam_cd_f64. */
 int pam_assemble_tiles_f64(int dim, int64_t S, const int64_t* row_off, const double* pts,
                            const int32_t* perm, const int64_t* dict_off, const int32_t* m_cur,
                            const double* centres, const double* widths, const int64_t* w_off,
@@ -177,8 +195,9 @@ int pam_cd_tiles_f64(int64_t S, const int64_t* order, const int64_t* row_off, co
                      const int64_t* w_off, const uint64_t* tile_mask, const int64_t* col_off,
                      const double* W, const double* lam1, const double* lam2, const double* tol,
                      const int32_t* max_iters, const int32_t* active, int32_t max_rows,
-                     double* beta, double* col_sq, int32_t* sweeps, int32_t* converged,
-                     double* objective, double* hist, const int64_t* hist_off, void* stream);
+                     int32_t max_m, double* beta, double* col_sq, int32_t* sweeps,
+                     int32_t* converged, double* objective, double* hist, const int64_t* hist_off,
+                     int32_t kernel, void* work, void* stream);
 
 /* ---- K2 + K2b': Gram products and the Gram-form CD (M < N) -----------------
  * pam_gram_f64: G_s = W_s^T W_s (symmetric, column-major at G + g_off[s],
@@ -189,7 +208,8 @@ int pam_cd_tiles_f64(int64_t S, const int64_t* order, const int64_t* row_off, co
  * same decisions and stop rule, M*M doubles streamed per sweep (vs N*M).
  * Writes beta, sweeps, converged (the objective is then evaluated exactly by
  * pam_cd_f64 with max_iters = 0, which computes 0.5|y - W beta|^2 + ...).
- * Requires M <= 512 and ldg <= 512. */
+ * Requires M <= 3072 (> 512 only sensible for <= 1 fit per SM).  `work`: the
+ * CD workspace (its first 4 bytes hold the work counter). */
 int pam_gram_f64(int64_t S, const int64_t* row_off, const int32_t* m_cur, const int64_t* dict_off,
                  const int64_t* w_off, const int32_t* ld, const int64_t* g_off, const int32_t* ldg,
                  const int32_t* active, int32_t max_m, const double* W, const double* y,
@@ -199,7 +219,7 @@ int pam_cd_gram_f64(int64_t S, const int64_t* order, const int64_t* dict_off, co
                     const double* col_sq, const double* lam1, const double* lam2,
                     const double* tol, const int32_t* max_iters, const int32_t* active,
                     int32_t max_m, double* beta, int32_t* sweeps, int32_t* converged,
-                    void* stream);
+                    void* work, void* stream);
 
 /* ---- K3: residual indicators + L2 misfit parts -----------------------------
  * Replaces residual_indicators (adaptive.py:133-138) with cell_quadrature

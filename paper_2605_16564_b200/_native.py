@@ -20,9 +20,8 @@ import numpy as np
 from .errors import NumericalError
 
 LIB_PATH = Path(__file__).resolve().parent / "libpam_b200.so"
-# A/B experiments only: PAM_LIB_PATH points at an alternative build of the same ABI
-if os.environ.get("PAM_LIB_PATH"):
-    LIB_PATH = Path(os.environ["PAM_LIB_PATH"])
+
+ABI_VERSION = 2  # PAM_ABI_VERSION of include/pam_b200.h
 
 # status codes (pam_b200.h)
 PAM_OK = 0
@@ -51,15 +50,16 @@ SIGNATURES = {
         [ctypes.c_int, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _i32, ctypes.c_int,
          _ptr, _ptr],
     ),
+    "pam_cd_workspace_bytes": (_i64, [_i64, _i64, _i32]),
     "pam_cd_f64": (
         ctypes.c_int,
         [_i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _i32,
-         _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr],
+         _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr],
     ),
     "pam_cd_ex_f64": (
         ctypes.c_int,
         [_i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _i32,
-         _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, ctypes.c_int, _ptr],
+         _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, ctypes.c_int, _ptr, _ptr],
     ),
     "pam_assemble_tiles_f64": (
         ctypes.c_int,
@@ -69,7 +69,7 @@ SIGNATURES = {
     "pam_cd_tiles_f64": (
         ctypes.c_int,
         [_i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr,
-         _ptr, _i32, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr],
+         _ptr, _i32, _i32, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _i32, _ptr, _ptr],
     ),
     "pam_gram_f64": (
         ctypes.c_int,
@@ -78,7 +78,7 @@ SIGNATURES = {
     "pam_cd_gram_f64": (
         ctypes.c_int,
         [_i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _i32,
-         _ptr, _ptr, _ptr, _ptr],
+         _ptr, _ptr, _ptr, _ptr, _ptr],
     ),
     "pam_residual_f64": (
         ctypes.c_int,
@@ -154,7 +154,7 @@ def load_library(path: Path | str | None = None):
             fn = getattr(lib, name)  # AttributeError = missing export
             fn.restype = res
             fn.argtypes = args
-        if lib.pam_abi_version() != 1:
+        if lib.pam_abi_version() != ABI_VERSION:
             raise NativeUnavailable("libpam_b200.so ABI version mismatch")
         if path is None:
             _lib = lib
@@ -325,8 +325,3 @@ def available() -> bool:
         return True
     except NativeUnavailable:
         return False
-
-
-def env_flag(name: str, default: bool = False) -> bool:
-    v = os.environ.get(name)
-    return default if v is None else v not in ("0", "", "false", "False")

@@ -10,15 +10,7 @@
 #include <string.h>
 
 #include <algorithm>
-#include <vector>
-
-extern "C" int pam_cd_ex_f64(int64_t S, const int64_t* order, const int64_t* row_off, double* y,
-                             const int64_t* dict_off, const int32_t* m_cur, const int64_t* w_off,
-                             const int32_t* ld, const double* W, const double* lam1,
-                             const double* lam2, const double* tol, const int32_t* max_iters,
-                             const int32_t* active, int32_t max_rows, double* beta, double* col_sq,
-                             int32_t* sweeps, int32_t* converged, double* objective, double* hist,
-                             const int64_t* hist_off, int flags, void* stream);
+#include <mutex>
 
 namespace pam {
 
@@ -35,18 +27,51 @@ int cuda_status(cudaError_t e, const char* where) {
   return PAM_ERR_CUDA;
 }
 
-// RAII device buffer for the host seams
-struct DevBuf {
+// Device arena of the host seams: one grow-only buffer per device, reused by
+// every call (no cudaMalloc/cudaFree per call).  The seams are synchronous and
+// serialised per device by the arena's mutex, like the reference's
+// one-loop-per-process model.
+constexpr int SEAM_DEVICES = 64;
+struct SeamArena {
+  std::mutex mu;
   void* p = nullptr;
-  cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, std::max<size_t>(bytes, 16)); }
-  ~DevBuf() {
-    if (p) cudaFree(p);
+  size_t cap = 0;
+};
+SeamArena g_arena[SEAM_DEVICES];
+
+struct SeamLease {
+  SeamArena* a = nullptr;
+  std::unique_lock<std::mutex> lock;
+  int acquire(size_t bytes) {
+    int dev = 0;
+    PAM_CUDA_CHECK(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= SEAM_DEVICES) {
+      set_last_error("device ordinal beyond the seam arena table");
+      return PAM_ERR_ARG;
+    }
+    a = &g_arena[dev];
+    lock = std::unique_lock<std::mutex>(a->mu);
+    if (a->cap < bytes) {
+      if (a->p) PAM_CUDA_CHECK(cudaFree(a->p));
+      a->p = nullptr;
+      a->cap = 0;
+      const size_t want = std::max<size_t>(bytes, size_t(1) << 20);
+      PAM_CUDA_CHECK(cudaMalloc(&a->p, want));
+      a->cap = want;
+    }
+    return PAM_OK;
   }
+  // carve consecutive 256-byte aligned pieces
+  size_t off = 0;
   template <class T>
-  T* as() const {
-    return static_cast<T*>(p);
+  T* take(size_t count) {
+    T* q = reinterpret_cast<T*>(static_cast<char*>(a->p) + off);
+    off += (std::max<size_t>(count * sizeof(T), 16) + 255) & ~size_t(255);
+    return q;
   }
 };
+
+inline size_t piece(size_t bytes) { return (std::max<size_t>(bytes, 16) + 255) & ~size_t(255); }
 
 }  // namespace pam
 
@@ -66,42 +91,43 @@ extern "C" int pam_cd_sweeps_host_f64(const double* W_fortran, int64_t n, int64_
     return PAM_ERR_ARG;
   if (n > pam_cd_max_rows()) return PAM_ERR_UNSUPPORTED;
   const int64_t ld = (n + 15) / 16 * 16;
-  DevBuf dW, dcs, db, dr, dmeta, dres, dh;
-  PAM_CUDA_CHECK(dW.alloc(sizeof(double) * ld * m));
-  PAM_CUDA_CHECK(dcs.alloc(sizeof(double) * m));
-  PAM_CUDA_CHECK(db.alloc(sizeof(double) * m));
-  PAM_CUDA_CHECK(dr.alloc(sizeof(double) * n));
-  PAM_CUDA_CHECK(dh.alloc(sizeof(double) * max_iters));
-  // meta: row_off[2], dict_off[1], w_off[1], hist_off[1] (int64); m_cur, ld, max_iters (int32)
-  PAM_CUDA_CHECK(dmeta.alloc(256));
-  PAM_CUDA_CHECK(dres.alloc(256));
-  PAM_CUDA_CHECK(cudaMemcpy2D(dW.p, ld * sizeof(double), W_fortran, n * sizeof(double),
-                              n * sizeof(double), m, cudaMemcpyHostToDevice));
-  PAM_CUDA_CHECK(cudaMemcpy(dcs.p, col_sq, sizeof(double) * m, cudaMemcpyHostToDevice));
-  PAM_CUDA_CHECK(cudaMemcpy(db.p, beta, sizeof(double) * m, cudaMemcpyHostToDevice));
-  PAM_CUDA_CHECK(cudaMemcpy(dr.p, r, sizeof(double) * n, cudaMemcpyHostToDevice));
+  const int64_t wsb = pam_cd_workspace_bytes(1, n, static_cast<int32_t>(std::min<int64_t>(n, INT32_MAX)));
   struct Meta {
     int64_t row_off[2], dict_off, w_off, hist_off;
     double lam1, lam2, tol;
     int32_t m_cur, ld, max_iters, pad;
   } meta{{0, n}, 0, 0, 0, lam1, lam2, tol, (int32_t)m, (int32_t)ld, (int32_t)max_iters, 0};
-  PAM_CUDA_CHECK(cudaMemcpy(dmeta.p, &meta, sizeof(meta), cudaMemcpyHostToDevice));
-  Meta* dm = dmeta.as<Meta>();
-  int32_t* res_i = dres.as<int32_t>();  // sweeps, converged
+  SeamLease L;
+  int rc = L.acquire(piece(sizeof(double) * ld * m) + piece(sizeof(double) * m) * 2 + piece(sizeof(double) * n) +
+                     piece(sizeof(double) * max_iters) + piece(sizeof(Meta)) + piece(64) + piece(wsb));
+  if (rc != PAM_OK) return rc;
+  double* dW = L.take<double>(ld * m);
+  double* dcs = L.take<double>(m);
+  double* db = L.take<double>(m);
+  double* dr = L.take<double>(n);
+  double* dh = L.take<double>(max_iters);
+  Meta* dm = L.take<Meta>(1);
+  int32_t* res_i = L.take<int32_t>(16);  // sweeps, converged, objective
+  void* work = L.take<char>(wsb);
+  PAM_CUDA_CHECK(cudaMemcpy2D(dW, ld * sizeof(double), W_fortran, n * sizeof(double),
+                              n * sizeof(double), m, cudaMemcpyHostToDevice));
+  PAM_CUDA_CHECK(cudaMemcpy(dcs, col_sq, sizeof(double) * m, cudaMemcpyHostToDevice));
+  PAM_CUDA_CHECK(cudaMemcpy(db, beta, sizeof(double) * m, cudaMemcpyHostToDevice));
+  PAM_CUDA_CHECK(cudaMemcpy(dr, r, sizeof(double) * n, cudaMemcpyHostToDevice));
+  PAM_CUDA_CHECK(cudaMemcpy(dm, &meta, sizeof(meta), cudaMemcpyHostToDevice));
   double* res_d = reinterpret_cast<double*>(res_i + 4);
-  int rc = pam_cd_ex_f64(1, nullptr, dm->row_off, dr.as<double>(), &dm->dict_off, &dm->m_cur,
-                         &dm->w_off, &dm->ld, dW.as<double>(), &dm->lam1, &dm->lam2, &dm->tol,
-                         &dm->max_iters, nullptr, (int32_t)n, db.as<double>(), dcs.as<double>(),
-                         res_i, res_i + 1, res_d, dh.as<double>(), &dm->hist_off,
-                         /*COLSQ_GIVEN|R_GIVEN|WRITE_R*/ 1 | 2 | 4, nullptr);
+  rc = pam_cd_ex_f64(1, nullptr, dm->row_off, dr, &dm->dict_off, &dm->m_cur, &dm->w_off, &dm->ld, dW,
+                     &dm->lam1, &dm->lam2, &dm->tol, &dm->max_iters, nullptr,
+                     static_cast<int32_t>(std::min<int64_t>(n, INT32_MAX)), db, dcs, res_i, res_i + 1, res_d, dh,
+                     &dm->hist_off, /*COLSQ_GIVEN|R_GIVEN|WRITE_R*/ 1 | 2 | 4, work, nullptr);
   if (rc != PAM_OK) return rc;
   PAM_CUDA_CHECK(cudaDeviceSynchronize());
   int32_t ri[2];
   PAM_CUDA_CHECK(cudaMemcpy(ri, res_i, sizeof(ri), cudaMemcpyDeviceToHost));
-  PAM_CUDA_CHECK(cudaMemcpy(beta, db.p, sizeof(double) * m, cudaMemcpyDeviceToHost));
-  PAM_CUDA_CHECK(cudaMemcpy(r, dr.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  PAM_CUDA_CHECK(cudaMemcpy(beta, db, sizeof(double) * m, cudaMemcpyDeviceToHost));
+  PAM_CUDA_CHECK(cudaMemcpy(r, dr, sizeof(double) * n, cudaMemcpyDeviceToHost));
   if (history)
-    PAM_CUDA_CHECK(cudaMemcpy(history, dh.p, sizeof(double) * ri[0], cudaMemcpyDeviceToHost));
+    PAM_CUDA_CHECK(cudaMemcpy(history, dh, sizeof(double) * ri[0], cudaMemcpyDeviceToHost));
   if (sweeps_out) *sweeps_out = ri[0];
   if (converged_out) *converged_out = ri[1];
   return PAM_OK;
@@ -113,26 +139,28 @@ extern "C" int pam_shepard_eval_host_f64(int dim, int64_t P, const double* pts, 
   if (dim < 1 || dim > 3 || P < 0 || M < 1 || !pts || !centres || !widths || !beta || !out)
     return PAM_ERR_ARG;
   if (P == 0) return PAM_OK;
-  DevBuf dp, dc, dw, db, dout, derr;
-  PAM_CUDA_CHECK(dp.alloc(sizeof(double) * P * dim));
-  PAM_CUDA_CHECK(dc.alloc(sizeof(double) * M * dim));
-  PAM_CUDA_CHECK(dw.alloc(sizeof(double) * M));
-  PAM_CUDA_CHECK(db.alloc(sizeof(double) * M));
-  PAM_CUDA_CHECK(dout.alloc(sizeof(double) * P));
-  PAM_CUDA_CHECK(derr.alloc(sizeof(int64_t) * 2));
-  PAM_CUDA_CHECK(cudaMemcpy(dp.p, pts, sizeof(double) * P * dim, cudaMemcpyHostToDevice));
-  PAM_CUDA_CHECK(cudaMemcpy(dc.p, centres, sizeof(double) * M * dim, cudaMemcpyHostToDevice));
-  PAM_CUDA_CHECK(cudaMemcpy(dw.p, widths, sizeof(double) * M, cudaMemcpyHostToDevice));
-  PAM_CUDA_CHECK(cudaMemcpy(db.p, beta, sizeof(double) * M, cudaMemcpyHostToDevice));
-  int rc = pam_err_reset(derr.as<int64_t>(), nullptr);
+  SeamLease L;
+  int rc = L.acquire(piece(sizeof(double) * P * dim) + piece(sizeof(double) * M * dim) +
+                     piece(sizeof(double) * M) * 2 + piece(sizeof(double) * P) + piece(16));
   if (rc != PAM_OK) return rc;
-  rc = pam_shepard_eval_f64(dim, P, dp.as<double>(), M, dc.as<double>(), dw.as<double>(),
-                            db.as<double>(), 0, dout.as<double>(), derr.as<int64_t>(), nullptr);
+  double* dp = L.take<double>(P * dim);
+  double* dc = L.take<double>(M * dim);
+  double* dw = L.take<double>(M);
+  double* db = L.take<double>(M);
+  double* dout = L.take<double>(P);
+  int64_t* derr = L.take<int64_t>(2);
+  PAM_CUDA_CHECK(cudaMemcpy(dp, pts, sizeof(double) * P * dim, cudaMemcpyHostToDevice));
+  PAM_CUDA_CHECK(cudaMemcpy(dc, centres, sizeof(double) * M * dim, cudaMemcpyHostToDevice));
+  PAM_CUDA_CHECK(cudaMemcpy(dw, widths, sizeof(double) * M, cudaMemcpyHostToDevice));
+  PAM_CUDA_CHECK(cudaMemcpy(db, beta, sizeof(double) * M, cudaMemcpyHostToDevice));
+  rc = pam_err_reset(derr, nullptr);
+  if (rc != PAM_OK) return rc;
+  rc = pam_shepard_eval_f64(dim, P, dp, M, dc, dw, db, 0, dout, derr, nullptr);
   if (rc != PAM_OK) return rc;
   PAM_CUDA_CHECK(cudaDeviceSynchronize());
   int64_t e[2];
-  PAM_CUDA_CHECK(cudaMemcpy(e, derr.p, sizeof(e), cudaMemcpyDeviceToHost));
-  PAM_CUDA_CHECK(cudaMemcpy(out, dout.p, sizeof(double) * P, cudaMemcpyDeviceToHost));
+  PAM_CUDA_CHECK(cudaMemcpy(e, derr, sizeof(e), cudaMemcpyDeviceToHost));
+  PAM_CUDA_CHECK(cudaMemcpy(out, dout, sizeof(double) * P, cudaMemcpyDeviceToHost));
   if (e[0] != 0) {
     if (err_index) *err_index = e[1];
     return (int)e[0];

@@ -31,7 +31,7 @@
 
 namespace pam {
 
-__device__ unsigned int g_cd_queue;
+constexpr int CD_REG_ROWS = 8192;  // rows a register-resident residual covers (cd_kernel, G = 8)
 
 enum : int { CD_COLSQ_GIVEN = 1, CD_R_GIVEN = 2, CD_WRITE_R = 4 };
 
@@ -62,6 +62,8 @@ struct CdArgs {
   const unsigned long long* tile_mask;
   const int64_t* col_off;
   const int32_t* perm;  // tile mode: packed position -> local row (nullable = identity)
+  unsigned* queue;      // work counter in the caller's workspace (zeroed by the launcher)
+  double* rbuf;         // large-fit residual scratch (sum N doubles, workspace)
 };
 
 // named barrier over the G warps of one subdomain group (G > 1 only)
@@ -69,12 +71,13 @@ __device__ __forceinline__ void group_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// R: rows per thread, STAGES: ring depth, WPC: warps per CTA, G: warps per
-// subdomain group (rows of a subdomain split over the G*32 threads).
-template <int R, int STAGES, int WPC, int G, bool TILES, bool KEEPW = true, bool LDGSTS = false>
+// Dense column-major design matrices (tau = 0, the Gram form's exact
+// objective pass, rows > 1024).  R: rows per thread, STAGES: ring depth,
+// WPC: warps per CTA, G: warps per subdomain group (rows of a subdomain split
+// over the G*32 threads).  Whole columns are staged HBM -> SMEM by
+// cp.async.bulk, STAGES ahead of the consumer.
+template <int R, int STAGES, int WPC, int G>
 __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
-  static_assert(!LDGSTS || (G == 1 && STAGES == 3), "LDGSTS staging: one warp, 3 stages");
-  static_assert(!TILES || G == 1, "tile-packed columns are consumed one warp per subdomain");
   constexpr int GT = G * 32;         // threads per group
   constexpr int LDMAX = R * GT;      // rows per ring slot
   constexpr int NGROUPS = WPC / G;
@@ -94,16 +97,15 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
                     NGROUPS * STAGES) +
                 grp * (2 * G + 1);  // double-buffered cross-warp partials + queue slot
   const int bar_id = 1 + grp;
-  // per-warp column-parameter block (G == 1): beta, col_sq, tile mask of the
-  // current 32-column chunk, read by warp-uniform smem broadcasts
+  // per-warp column-parameter block (G == 1): beta, col_sq, 1/(col_sq+lam2)
+  // of the current 32-column chunk, read by warp-uniform smem broadcasts
   constexpr bool PSM = (G == 1);
   double* prm_base = reinterpret_cast<double*>(smem_raw) +
                      (static_cast<size_t>(NGROUPS) * STAGES * LDMAX) + NGROUPS * STAGES +
                      NGROUPS * (2 * G + 1);
-  double* pb = prm_base + grp * 128;
+  double* pb = prm_base + grp * 96;
   double* pc = pb + 32;
   double* pinv = pb + 64;  // 1 / (col_sq + lam2): division by reciprocal + one FMA correction
-  unsigned* pm = reinterpret_cast<unsigned*>(pb + 96);
 
   auto sync_group = [&]() {
     if (G == 1) __syncwarp();
@@ -149,56 +151,20 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
       const bool r_given = (a.flags & CD_R_GIVEN) != 0;
       const bool prologue = need_colsq || !r_given;
 
-      // residual / targets into registers (thread gt owns rows gt + GT*k);
-      // in tile mode position p = lane + 32k holds local row perm[p]
+      // residual / targets into registers (thread gt owns rows gt + GT*k)
       double r[R];
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         const int p = gt + GT * k;
-        const int row = (TILES && a.perm) ? (p < N ? a.perm[r0 + p] : 0) : p;
-        r[k] = (p < N) ? a.y[r0 + row] : 0.0;
+        r[k] = (p < N) ? a.y[r0 + p] : 0.0;
       }
-
-      // per-column packing parameters for the ISSUE pointer (tile mode)
-      int iss_base = -64;
-      int64_t iss_off_l = 0;
-      unsigned long long iss_mask_l = 0;
 
       // continuous column stream: [prologue M columns] + max_iters * M columns
       const int64_t total = (prologue ? (int64_t)M : 0) + (int64_t)max_iters * M;
       int64_t issued = 0;
       int next_col = 0;
       auto issue_one = [&]() {
-        if (TILES) {
-          const int cbase = next_col & ~31;
-          if (cbase != iss_base) {  // warp-uniform reload of 32 columns' packing
-            iss_base = cbase;
-            const int c = cbase + lane;
-            iss_off_l = (c < M) ? a.col_off[doff + c] : 0;
-            iss_mask_l = (c < M) ? a.tile_mask[doff + c] : 0ull;
-          }
-          const int off = __shfl_sync(0xffffffffu, static_cast<int>(iss_off_l), next_col & 31);
-          unsigned long long mk;
-          if (R <= 32) mk = __shfl_sync(0xffffffffu, static_cast<unsigned>(iss_mask_l), next_col & 31);
-          else mk = __shfl_sync(0xffffffffu, iss_mask_l, next_col & 31);
-          const uint32_t nb = static_cast<uint32_t>(__popcll(mk)) * 32u * sizeof(double);
-          if (LDGSTS) {
-            // per-lane 16-byte async copies of the packed column (no TMA unit)
-            double* dst = ring + (g_issue % STAGES) * LDMAX;
-            const double* src = Ws + off;
-            const int pieces = static_cast<int>(nb / 16u);
-            for (int i = lane; i < pieces; i += 32) cp_async16(dst + 2 * i, src + 2 * i);
-            cp_async_commit();
-          } else if (lane == 0) {
-            const int st = g_issue % STAGES;
-            if (nb) {
-              mbar_arrive_expect_tx(&bars[st], nb);
-              tma_load_1d(ring + st * LDMAX, Ws + off, nb, &bars[st]);
-            } else {
-              mbar_arrive(&bars[st]);  // empty column: complete the phase without data
-            }
-          }
-        } else if (gt == 0) {
+        if (gt == 0) {
           const int st = g_issue % STAGES;
           mbar_arrive_expect_tx(&bars[st], dense_bytes);
           tma_load_1d(ring + st * LDMAX, Ws + (int64_t)next_col * ld, dense_bytes, &bars[st]);
@@ -209,104 +175,38 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
       };
       auto wait_one = [&]() -> const double* {
         const int st = g_cons % STAGES;
-        if (LDGSTS) {
-          const int ahead = static_cast<int>(g_issue - g_cons) - 1;  // groups that may stay in flight
-          if (ahead >= 2) cp_async_wait<2>();
-          else if (ahead == 1) cp_async_wait<1>();
-          else cp_async_wait<0>();
-          __syncwarp();
-        } else {
-          mbar_wait(&bars[st], (g_cons / STAGES) & 1u);
-        }
+        mbar_wait(&bars[st], (g_cons / STAGES) & 1u);
         ++g_cons;
         return ring + st * LDMAX;
       };
       // Column staging: the column's entries for this thread's rows go to
       // registers once and serve both the dot and the AXPY.  Branch-free: rows
-      // past N (dense) or tiles not stored (tile mode) read an in-bounds smem
-      // word and select 0, so they contribute exactly nothing.
-      double w[KEEPW ? R : 1];
-      const double* cur_col = nullptr;
-      unsigned long long cur_mk = 0ull;
-      auto load_col = [&](const double* col, unsigned long long mk) {
-        cur_col = col;
-        cur_mk = mk;
-        if (!KEEPW) return;
-        if (TILES) {
-          // Tiles in groups of four with warp-uniform fast paths: RCB ordering
-          // makes kept tiles cluster, so most groups are all-kept (contiguous
-          // loads, no selects) or all-dropped (zeros).  Any mask shape.
-          int slot = 0;
+      // past N read an in-bounds smem word and select 0.
+      double w[R];
+      auto load_col = [&](const double* col) {
 #pragma unroll
-          for (int g = 0; g < (R + 3) / 4; ++g) {
-            const int cnt = (4 * g + 4 <= R) ? 4 : (R - 4 * g);
-            const unsigned full = (1u << cnt) - 1u;
-            const unsigned nib = static_cast<unsigned>(mk >> (4 * g)) & full;
-            if (nib == full) {
-#pragma unroll
-              for (int u = 0; u < 4; ++u)
-                if (u < cnt) w[4 * g + u] = col[32 * (slot + u) + lane];
-              slot += cnt;
-            } else if (nib == 0u) {
-#pragma unroll
-              for (int u = 0; u < 4; ++u)
-                if (u < cnt) w[4 * g + u] = 0.0;
-            } else {
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                if (u < cnt) {
-                  const int bit = static_cast<int>((nib >> u) & 1u);
-                  const double v = col[32 * slot + lane];  // slot <= k < R: inside the ring slot
-                  w[4 * g + u] = bit ? v : 0.0;
-                  slot += bit;
-                }
-              }
-            }
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < R; ++k) {
-            const double v = col[gt + GT * k];
-            w[k] = (gt + GT * k < N) ? v : 0.0;
-          }
+        for (int k = 0; k < R; ++k) {
+          const double v = col[gt + GT * k];
+          w[k] = (gt + GT * k < N) ? v : 0.0;
         }
-      };
-      // entry k of the current column for this thread (0 when absent)
-      auto wk = [&](int k, int& slot) -> double {
-        if (KEEPW) return w[KEEPW ? k : 0];
-        if (TILES) {
-          const int bit = static_cast<int>((cur_mk >> k) & 1ull);
-          const double v = cur_col[32 * slot + lane];
-          slot += bit;
-          return bit ? v : 0.0;
-        }
-        const double v = cur_col[gt + GT * k];
-        return (gt + GT * k < N) ? v : 0.0;
       };
       auto col_dot = [&]() -> double {
         double d0 = 0.0, d1 = 0.0;  // two independent chains halve the FMA latency
-        int slot = 0;
 #pragma unroll
         for (int k = 0; k < R; ++k) {
-          const double v = wk(k, slot);
-          if (k & 1) d1 = fma(v, r[k], d1);
-          else d0 = fma(v, r[k], d0);
+          if (k & 1) d1 = fma(w[k], r[k], d1);
+          else d0 = fma(w[k], r[k], d0);
         }
         return d0 + d1;
       };
       auto col_axpy = [&](double d) {
-        int slot = 0;
 #pragma unroll
-        for (int k = 0; k < R; ++k) r[k] = fma(-d, wk(k, slot), r[k]);
+        for (int k = 0; k < R; ++k) r[k] = fma(-d, w[k], r[k]);
       };
       auto col_sumsq = [&]() -> double {
         double p = 0.0;
-        int slot = 0;
 #pragma unroll
-        for (int k = 0; k < R; ++k) {
-          const double v = wk(k, slot);
-          p = fma(v, v, p);
-        }
+        for (int k = 0; k < R; ++k) p = fma(w[k], w[k], p);
         return p;
       };
       for (int q = 0; q < STAGES && issued < total; ++q) issue_one();
@@ -314,27 +214,20 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
 
       // ---- prologue: col_sq (elastic_net.py:85) and r = y - W beta0 (94)
       if (prologue) {
-        for (int cb = 0; cb < M; cb += 32) {
-          const int nc = min(32, M - cb);
-          unsigned long long ml = 0ull;
-          if (TILES && lane < nc) ml = a.tile_mask[doff + cb + lane];
-          for (int t = 0; t < nc; ++t) {
-            const int j = cb + t;
-            const unsigned long long mk = TILES ? __shfl_sync(0xffffffffu, ml, t) : 0ull;
-            const double* col = wait_one();
-            ++consumed;
-            load_col(col, mk);
-            if (need_colsq) {
-              double p = group_sum(col_sumsq());
-              if (gt == 0) a.col_sq[doff + j] = p;
-            }
-            if (!r_given) {
-              const double b0 = a.beta[doff + j];
-              if (b0 != 0.0) col_axpy(b0);
-            }
-            sync_group();
-            if (issued < total) issue_one();
+        for (int j = 0; j < M; ++j) {
+          const double* col = wait_one();
+          ++consumed;
+          load_col(col);
+          if (need_colsq) {
+            double p = group_sum(col_sumsq());
+            if (gt == 0) a.col_sq[doff + j] = p;
           }
+          if (!r_given) {
+            const double b0 = a.beta[doff + j];
+            if (b0 != 0.0) col_axpy(b0);
+          }
+          sync_group();
+          if (issued < total) issue_one();
         }
         __threadfence_block();  // col_sq stores visible to the whole group
         sync_group();
@@ -351,7 +244,6 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
           const int nc = min(32, M - cb);
           // every warp of the group holds the same 32 column parameters
           double bl = 0.0, csl = 0.0;
-          unsigned long long ml = 0ull;
           if (PSM) {
             __syncwarp();
             if (lane < nc) {
@@ -360,24 +252,16 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
               pc[lane] = csv;
               const double dnv = __dadd_rn(csv, lam2);
               pinv[lane] = dnv > 0.0 ? __ddiv_rn(1.0, dnv) : 0.0;
-              if (TILES) pm[lane] = static_cast<unsigned>(a.tile_mask[doff + cb + lane]);
             }
             __syncwarp();
           } else if (lane < nc) {
             bl = a.beta[doff + cb + lane];
             csl = a.col_sq[doff + cb + lane];
-            if (TILES) ml = a.tile_mask[doff + cb + lane];
           }
           for (int t = 0; t < nc; ++t) {
-            unsigned long long mk = 0ull;
-            if (TILES) {
-              if (PSM) mk = pm[t];
-              else if (R <= 32) mk = __shfl_sync(0xffffffffu, static_cast<unsigned>(ml), t);
-              else mk = __shfl_sync(0xffffffffu, ml, t);
-            }
             const double* col = wait_one();
             ++consumed;
-            load_col(col, mk);
+            load_col(col);
             const double dot = group_sum(col_dot());
             const double b_old = PSM ? pb[t] : __shfl_sync(0xffffffffu, bl, t);
             const double cs = PSM ? pc[t] : __shfl_sync(0xffffffffu, csl, t);
@@ -457,12 +341,6 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
                         __dmul_rn(__dmul_rn(0.5, lam2), l2));
       }
       // drain speculative prefetches of the sweep that will not run
-      if (LDGSTS) {
-        cp_async_wait<0>();
-        __syncwarp();
-        g_cons += static_cast<uint32_t>(issued - consumed);
-        consumed = issued;
-      }
       while (consumed < issued) {
         (void)wait_one();
         ++consumed;
@@ -472,7 +350,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
 #pragma unroll
         for (int k = 0; k < R; ++k) {
           const int p = gt + GT * k;
-          if (p < N) a.y[r0 + ((TILES && a.perm) ? a.perm[r0 + p] : p)] = r[k];
+          if (p < N) a.y[r0 + p] = r[k];
         }
       }
       if (gt == 0) {
@@ -483,7 +361,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
     }
     // next item: dynamic queue after the static first pass
     unsigned nxt = 0;
-    if (gt == 0) nxt = atomicAdd(&g_cd_queue, 1u) + total_groups;
+    if (gt == 0) nxt = atomicAdd(a.queue, 1u) + total_groups;
     if (G == 1) {
       item = __shfl_sync(0xffffffffu, nxt, 0);
     } else {
@@ -496,48 +374,40 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
 }
 
 // ----------------------------------------------------------------------------
-// Lean tile-stream CD (default for tile-packed batches of <= 1024 rows).
+// Lean tile-stream CD (one fit per warp, tile-packed batches of <= 1024 rows).
 //
-// Same semantics and the same one-warp-per-fit / staged-ring design as
-// cd_kernel<..., TILES=true>, with the per-column instruction count cut down
-// (the generic tile kernel is issue-bound; profiles/r01_*):
-//  * columns are at most two contiguous runs of kept tiles (tiles.cu run
-//    cover), staged packed at the slot start; a lane addresses its tile with
-//    one of two bases instead of per-tile slot counting;
+// Same semantics as cd_kernel over the tile-packed design matrices of
+// tiles.cu, with the per-column instruction count cut down (the generic
+// per-column loop is issue-bound; profiles/r01_*):
+//  * every column is ONE contiguous run of kept 32-row tiles [a0, a0+la),
+//    staged packed at the slot start by one cp.async.bulk; a lane addresses
+//    its tile with one base and one predicate, out-of-run tiles read a
+//    CTA-wide zero block;
 //  * paired-row layout (R even): lane l owns packed rows 64q + 2l + {0,1}, so
 //    one 16-byte shared load feeds two registers (tile 2q + (l >> 4));
 //  * per-32-column chunk parameters (beta, col_sq, 1/(col_sq+lam2), run
 //    code, packed offset) are prefetched into registers one chunk ahead and
 //    published to a per-warp smem block: no global load on the column loop;
-//  * the issue path is one LDS + expect_tx + one bulk copy by lane 0 (TMA), or
-//    (CPA) per-lane 16-byte cp.async copies of exactly the words the lane
-//    reads later, which needs no mbarrier and no cross-lane hand-off.
-// Measured alternatives: placing tiles at their dense position
-// and clearing stale tiles (by zero-page bulk copies or by shared stores) so
-// loads need no predicates was 12-14% slower than predicated packed loads.
+//  * the issue path is one LDS + expect_tx + one bulk copy by lane 0.
+// Measured alternatives: per-lane cp.async staging, two-run
+// masks, dense tile placement with stale-tile clears and deeper rings were
+// all slower and have been removed.
 
-// Run code of a tile mask made of at most two runs (tiles.cu run_cover):
-// a0 | la << 8 | b0 << 16 | lb << 24  (run A = tiles [a0, a0+la), B after it)
+// Run code of a tile mask made of one contiguous run (tiles.cu run_cover):
+// a0 | la << 8  (run = tiles [a0, a0+la))
 __device__ __forceinline__ int tile_code(unsigned long long mk) {
   if (mk == 0ull) return 0;
   const int a0 = __ffsll(static_cast<long long>(mk)) - 1;
-  const unsigned long long x = ~(mk >> a0);
-  const int la = x ? (__ffsll(static_cast<long long>(x)) - 1) : 64 - a0;
-  const unsigned long long rest = (la >= 64) ? 0ull : (mk & ~(((1ull << la) - 1ull) << a0));
-  const int b0 = rest ? (__ffsll(static_cast<long long>(rest)) - 1) : 0;
-  return a0 | (la << 8) | (b0 << 16) | (__popcll(rest) << 24);
+  return a0 | (__popcll(mk) << 8);
 }
-__device__ __forceinline__ int code_tiles(int code) {
-  return ((code >> 8) & 0xff) + ((code >> 24) & 0xff);
-}
+__device__ __forceinline__ int code_tiles(int code) { return (code >> 8) & 0xff; }
 
-template <int R, int STAGES, int WPC, bool CPA, int RUNS>
+template <int R, int STAGES, int WPC>
 __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
   constexpr int SLOT = R * 32;  // doubles per ring slot (one dense column)
   constexpr int PBLK = 144;     // doubles per warp: pb/pc/pinv[32] + pk/ioff/icode[32]
   static_assert(R <= 32 && STAGES <= 8, "lean tile CD envelope");
   constexpr bool VEC = (R % 2) == 0;
-  static_assert(!CPA || VEC, "per-lane async copies need the paired-row layout");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -571,7 +441,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
   __syncthreads();
 
   int st = 0;       // consumer ring slot
-  uint32_t ph = 0;  // its mbarrier phase parity (TMA staging)
+  uint32_t ph = 0;  // its mbarrier phase parity
   int ist = 0;      // issue ring slot
   unsigned item = warp * gridDim.x + blockIdx.x;
   const unsigned total_warps = gridDim.x * WPC;
@@ -625,25 +495,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
           __syncwarp();
           fetch_issue(next_col + 32 < M ? next_col + 32 : 0);
         }
-        if (CPA) {
-          // per-lane 16-byte async copies of exactly the words this lane reads
-          // later: pair q covers tile 2q + half at packed slot (t - a0) or
-          // (la + t - b0)
-          const int code = icode[c];
-          const int a0 = code & 0xff, la = (code >> 8) & 0xff;
-          const int b0 = (code >> 16) & 0xff, lb = code >> 24;
-          const int offA = ioff[c] - 32 * a0 + 2 * lane, offB = ioff[c] + 32 * (la - b0) + 2 * lane;
-          double* slot = ring + ist * SLOT;
-#pragma unroll
-          for (int q = 0; q < R / 2; ++q) {
-            const int t = 2 * q + half;
-            const bool inA = static_cast<unsigned>(t - a0) < static_cast<unsigned>(la);
-            const bool inB = static_cast<unsigned>(t - b0) < static_cast<unsigned>(lb);
-            const int o = (inA ? offA : offB) + 64 * q;
-            if (inA || inB) cp_async16_dep(slot + (o - ioff[c]), Ws + o, dep);
-          }
-          cp_async_commit();
-        } else if (lane == 0) {
+        if (lane == 0) {
           const int code = icode[c];
           const uint32_t bytes = static_cast<uint32_t>(code_tiles(code)) * 256u;
           const uint32_t bar = bar_s + ist * 8;
@@ -658,15 +510,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
         ++issued;
         if (++next_col == M) next_col = 0;
       };
-      if (CPA) {
-        st = ist = 0;  // the previous item drained every copy group
-        for (int q = 0; q < STAGES; ++q) {
-          if (issued < total) issue_one(0.0);
-          else cp_async_commit();  // empty group: one group per stream position
-        }
-      } else {
-        for (int q = 0; q < STAGES && issued < total; ++q) issue_one(0.0);
-      }
+      for (int q = 0; q < STAGES && issued < total; ++q) issue_one(0.0);
 
       // ---- consumer side
       int consumed = 0;
@@ -674,49 +518,24 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
       double w[R];
       auto load_w = [&](int code) {
         const double* col = ring + st * SLOT;
-        if (CPA) cp_async_wait<STAGES - 1>();  // this lane's copies of the oldest group
-        else if (!ready) mbar_wait_s(bar_s + st * 8, ph);
+        if (!ready) mbar_wait_s(bar_s + st * 8, ph);
         const int a0 = code & 0xff, la = (code >> 8) & 0xff;
-        const int b0 = (code >> 16) & 0xff, lb = code >> 24;
-        if (VEC && !CPA) {
+        if (VEC) {
           // unconditional 16-byte shared loads; out-of-run tiles are redirected
           // to the zero block (one select per tile pair, no zeroing moves)
           const uint32_t cA = ring_s + st * (SLOT * 8) + 16u * lane - 256u * a0;
-          const uint32_t cB = ring_s + st * (SLOT * 8) + 16u * lane + 256u * (la - b0);
-          const int hA = half - a0, hB = half - b0;
+          const int hA = half - a0;
 #pragma unroll
           for (int q = 0; q < R / 2; ++q) {
             const bool inA = static_cast<unsigned>(hA + 2 * q) < static_cast<unsigned>(la);
-            uint32_t ad;
-            if (RUNS == 1) {
-              ad = inA ? cA : zero_s;
-            } else {
-              const bool inB = static_cast<unsigned>(hB + 2 * q) < static_cast<unsigned>(lb);
-              ad = inA ? cA : (inB ? cB : zero_s);
-            }
-            lds_v2(ad + 512u * q, w[2 * q], w[2 * q + 1]);
-          }
-        } else if (VEC) {
-          const double* bA = col - 32 * a0 + 2 * lane;
-          const double* bB = col + 32 * (la - b0) + 2 * lane;
-#pragma unroll
-          for (int q = 0; q < R / 2; ++q) {
-            const int t = 2 * q + half;
-            const bool inA = static_cast<unsigned>(t - a0) < static_cast<unsigned>(la);
-            const bool inB = static_cast<unsigned>(t - b0) < static_cast<unsigned>(lb);
-            const double2* src = reinterpret_cast<const double2*>((inA ? bA : bB) + 64 * q);
-            const double2 v = (inA || inB) ? *src : make_double2(0.0, 0.0);
-            w[2 * q] = v.x;
-            w[2 * q + 1] = v.y;
+            lds_v2((inA ? cA : zero_s) + 512u * q, w[2 * q], w[2 * q + 1]);
           }
         } else {
           const double* bA = col - 32 * a0 + lane;
-          const double* bB = col + 32 * (la - b0) + lane;
 #pragma unroll
           for (int k = 0; k < R; ++k) {
             const bool inA = static_cast<unsigned>(k - a0) < static_cast<unsigned>(la);
-            const bool inB = static_cast<unsigned>(k - b0) < static_cast<unsigned>(lb);
-            w[k] = (inA || inB) ? (inA ? bA : bB)[32 * k] : 0.0;
+            w[k] = inA ? bA[32 * k] : 0.0;
           }
         }
       };
@@ -724,7 +543,6 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
       // `dep`, a value computed from the loaded words) and step the ring
       auto advance = [&](double dep) {
         if (issued < total) issue_one(dep);
-        else if (CPA) cp_async_commit();
         if (++st == STAGES) {
           st = 0;
           ph ^= 1u;
@@ -732,7 +550,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
         ++consumed;
         // non-blocking look at the next slot now, so the barrier round trip
         // overlaps the reduction and update of this column
-        if (!CPA) ready = (consumed < issued) && mbar_test_s(bar_s + st * 8, ph);
+        ready = (consumed < issued) && mbar_test_s(bar_s + st * 8, ph);
       };
 
       // prologue: col_sq (elastic_net.py:85) and r = y - W beta0 (elastic_net.py:94)
@@ -778,9 +596,6 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
       fetch_params(0);
       int sweeps_done = 0, conv = 0;
       double obj = 0.0;
-#ifdef PAM_CD_PAD
-      unsigned pad0 = lane, pad1 = lane + 1, pad2 = lane + 2, pad3 = lane + 3;
-#endif
       for (int sw = 0; sw < max_iters; ++sw) {
         double max_delta = 0.0, acc_l1 = 0.0, acc_l2 = 0.0, acc_max = 0.0;
         for (int cb = 0; cb < M; cb += 32) {
@@ -831,17 +646,6 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
             if (lane == 0) pb[t] = b_new;
             const double ad = fabs(d);
             max_delta = ad > max_delta ? ad : max_delta;  // fmax without the NaN fix-up
-#ifdef PAM_CD_PAD
-            // diagnostic build (-DPAM_CD_PAD=n): n independent,
-            // non-foldable integer instructions per column
-#pragma unroll
-            for (int u = 0; u < PAM_CD_PAD / 4; ++u) {
-              pad0 = pad0 * pad0 + (2u * u + 1u);
-              pad1 = pad1 * pad1 + (2u * u + 3u);
-              pad2 = pad2 * pad2 + (2u * u + 5u);
-              pad3 = pad3 * pad3 + (2u * u + 7u);
-            }
-#endif
           }
           __syncwarp();
           if (lane < nc) {
@@ -888,14 +692,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
         obj = __dadd_rn(__dadd_rn(__dmul_rn(0.5, rss), __dmul_rn(lam1, l1)),
                         __dmul_rn(__dmul_rn(0.5, lam2), l2));
       }
-#ifdef PAM_CD_PAD
-      if ((pad0 ^ pad1 ^ pad2 ^ pad3) == 0x12345679u) a.sweeps[0] = -1;  // keeps the padding live
-#endif
       // drain the prefetched columns of the sweep that will not run
-      if (CPA) {
-        cp_async_wait<0>();
-        consumed = issued;
-      }
       while (consumed < issued) {
         mbar_wait_s(bar_s + st * 8, ph);
         if (++st == STAGES) {
@@ -912,7 +709,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
       }
     }
     unsigned nxt = 0;
-    if (lane == 0) nxt = atomicAdd(&g_cd_queue, 1u) + total_warps;
+    if (lane == 0) nxt = atomicAdd(a.queue, 1u) + total_warps;
     item = __shfl_sync(0xffffffffu, nxt, 0);
   }
 }
@@ -946,7 +743,7 @@ __device__ __forceinline__ double half_max(double v) {
   return v;
 }
 
-template <int R, int STAGES, int WPC, int RUNS>
+template <int R, int STAGES, int WPC>
 __global__ void __launch_bounds__(WPC * 32, 1) cd_dual_kernel(const CdArgs a) {
   constexpr int SLOTH = R * 16;  // doubles per half slot (one column of <= 16 R rows)
   constexpr int PBLK = 144;      // doubles per warp: pb/pc/pinv[32] + pk/ioff/icode[32] (index half*16 + c)
@@ -1072,20 +869,11 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_dual_kernel(const CdArgs a) {
     auto load_w = [&](int code) {
       if (!ready) mbar_wait_s(bar_s + st * 8, ph);
       const int a0 = code & 0xff, la = (code >> 8) & 0xff;
-      const int b0 = (code >> 16) & 0xff, lb = code >> 24;
       const uint32_t cA = ring_h + st * SLOT_B + 16u * hl - 256u * a0;
-      const uint32_t cB = ring_h + st * SLOT_B + 16u * hl + 256u * (la - b0);
 #pragma unroll
       for (int q = 0; q < R / 2; ++q) {
         const bool inA = static_cast<unsigned>(q - a0) < static_cast<unsigned>(la);
-        uint32_t ad;
-        if (RUNS == 1) {
-          ad = inA ? cA : zero_s;
-        } else {
-          const bool inB = static_cast<unsigned>(q - b0) < static_cast<unsigned>(lb);
-          ad = inA ? cA : (inB ? cB : zero_s);
-        }
-        lds_v2(ad + 256u * q, w[2 * q], w[2 * q + 1]);
+        lds_v2((inA ? cA : zero_s) + 256u * q, w[2 * q], w[2 * q + 1]);
       }
     };
     auto advance = [&](double dep) {
@@ -1255,7 +1043,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_dual_kernel(const CdArgs a) {
       a.objective[s] = obj;
     }
     unsigned nxt = 0;
-    if (lane == 0) nxt = atomicAdd(&g_cd_queue, 1u) + total_warps;
+    if (lane == 0) nxt = atomicAdd(a.queue, 1u) + total_warps;
     item = __shfl_sync(0xffffffffu, nxt, 0);
   }
 }
@@ -1538,9 +1326,187 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_pipe_kernel(const CdArgs a, in
       }
     }
     unsigned nxt = 0;
-    if (lane == 0) nxt = atomicAdd(&g_cd_queue, 1u) + total_warps;
+    if (lane == 0) nxt = atomicAdd(a.queue, 1u) + total_warps;
     item = __shfl_sync(0xffffffffu, nxt, 0);
   }
+}
+
+// ----------------------------------------------------------------------------
+// Large fits (N > 8192 rows, dense): one 512-thread CTA per fit, the residual
+// in a global scratch (each thread owns rows tid + 512 k, L2-resident), design
+// columns read straight from HBM (coalesced), a fixed-order CTA reduction per
+// column.  Same arithmetic as cd_kernel; lifts the row envelope of fit()
+// (elastic_net.py:66-110 has none).
+constexpr int LG_THREADS = 512;
+__global__ void __launch_bounds__(LG_THREADS) cd_large_kernel(const CdArgs a) {
+  __shared__ double red[2][LG_THREADS / 32];
+  __shared__ unsigned nxt_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int buf = 0;
+  auto cta_sum = [&](double v) -> double {
+    v = warp_sum(v);
+    if (lane == 0) red[buf][warp] = v;
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < LG_THREADS / 32; ++w) t += red[buf][w];
+    buf ^= 1;  // the next reduction writes the other buffer: one barrier per sum
+    return t;
+  };
+  unsigned item = blockIdx.x;
+  while (item < a.S) {
+    const int64_t s = a.order ? a.order[item] : static_cast<int64_t>(item);
+    if (a.active == nullptr || a.active[s] != 0) {
+      const int64_t r0 = a.row_off[s];
+      const int N = static_cast<int>(a.row_off[s + 1] - r0);
+      const int M = a.m_cur[s];
+      const int64_t doff = a.dict_off[s];
+      const double* Ws = a.W + a.w_off[s];
+      const int64_t ld = a.ld[s];
+      const double lam1 = a.lam1[s], lam2 = a.lam2[s], tol = a.tol[s];
+      const int max_iters = a.max_iters[s];
+      const bool need_colsq = !(a.flags & CD_COLSQ_GIVEN);
+      const bool r_given = (a.flags & CD_R_GIVEN) != 0;
+      double* r = a.rbuf + r0;
+      for (int i = tid; i < N; i += LG_THREADS) r[i] = a.y[r0 + i];
+      if (need_colsq || !r_given) {
+        for (int j = 0; j < M; ++j) {
+          const double* col = Ws + (int64_t)j * ld;
+          if (need_colsq) {
+            double p = 0.0;
+            for (int i = tid; i < N; i += LG_THREADS) p = fma(col[i], col[i], p);
+            p = cta_sum(p);
+            if (tid == 0) a.col_sq[doff + j] = p;
+          }
+          if (!r_given) {
+            const double b0 = a.beta[doff + j];
+            if (b0 != 0.0)
+              for (int i = tid; i < N; i += LG_THREADS) r[i] = fma(-b0, col[i], r[i]);
+          }
+        }
+        __syncthreads();
+      }
+      int sweeps_done = 0, conv = 0;
+      double obj = 0.0;
+      for (int sw = 0; sw < max_iters; ++sw) {
+        double max_delta = 0.0, l1 = 0.0, l2 = 0.0, mabs = 0.0;
+        for (int j = 0; j < M; ++j) {
+          const double* col = Ws + (int64_t)j * ld;
+          double p = 0.0;
+          for (int i = tid; i < N; i += LG_THREADS) p = fma(col[i], r[i], p);
+          const double dot = cta_sum(p);
+          const double b_old = a.beta[doff + j];
+          const double cs = a.col_sq[doff + j];
+          const double dn = __dadd_rn(cs, lam2);
+          const double z = __dadd_rn(__dmul_rn(cs, b_old), dot);
+          double b_new = 0.0;
+          if (dn > 0.0) {
+            double mag = __dsub_rn(fabs(z), lam1);
+            if (mag < 0.0) mag = 0.0;
+            b_new = __ddiv_rn(z >= 0.0 ? mag : -mag, dn);
+          }
+          const double d = __dsub_rn(b_new, b_old);
+          if (d != 0.0)
+            for (int i = tid; i < N; i += LG_THREADS) r[i] = fma(-d, col[i], r[i]);
+          __syncthreads();  // every thread read beta[j] before it is replaced
+          if (tid == 0) a.beta[doff + j] = b_new;
+          max_delta = fmax(max_delta, fabs(d));
+          const double ab = fabs(b_new);
+          l1 += ab;
+          l2 = fma(b_new, b_new, l2);
+          mabs = fmax(mabs, ab);
+        }
+        double rr = 0.0;
+        for (int i = tid; i < N; i += LG_THREADS) rr = fma(r[i], r[i], rr);
+        const double rss = cta_sum(rr);
+        obj = __dadd_rn(__dadd_rn(__dmul_rn(0.5, rss), __dmul_rn(lam1, l1)),
+                        __dmul_rn(__dmul_rn(0.5, lam2), l2));
+        if (a.hist != nullptr && tid == 0) a.hist[a.hist_off[s] + sw] = obj;
+        sweeps_done = sw + 1;
+        if (max_delta <= __dmul_rn(tol, fmax(mabs, 1.0))) {
+          conv = 1;
+          break;
+        }
+      }
+      if (max_iters == 0) {
+        double rr = 0.0, q1 = 0.0, q2 = 0.0;
+        for (int i = tid; i < N; i += LG_THREADS) rr = fma(r[i], r[i], rr);
+        for (int j = tid; j < M; j += LG_THREADS) {
+          const double b = a.beta[doff + j];
+          q1 += fabs(b);
+          q2 = fma(b, b, q2);
+        }
+        const double rss = cta_sum(rr);
+        const double t1 = cta_sum(q1);
+        const double t2 = cta_sum(q2);
+        obj = __dadd_rn(__dadd_rn(__dmul_rn(0.5, rss), __dmul_rn(lam1, t1)),
+                        __dmul_rn(__dmul_rn(0.5, lam2), t2));
+      }
+      if (a.flags & CD_WRITE_R)
+        for (int i = tid; i < N; i += LG_THREADS) a.y[r0 + i] = r[i];
+      if (tid == 0) {
+        a.sweeps[s] = sweeps_done;
+        a.converged[s] = conv;
+        a.objective[s] = obj;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) nxt_s = atomicAdd(a.queue, 1u) + gridDim.x;
+    __syncthreads();
+    item = nxt_s;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// launchers.  The dynamic shared-memory attribute is set on every launch (it
+// is per device and per function; the call is cheap), so one process may
+// drive several GPUs.
+
+inline int sm_count() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+template <typename K>
+int launch_persistent(K kernel, const CdArgs& a, int64_t units, int threads, size_t smem,
+                      cudaStream_t stream, const char* what) {
+  PAM_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  PAM_CUDA_CHECK(cudaMemsetAsync(a.queue, 0, sizeof(unsigned), stream));
+  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(sm_count(), units));
+  kernel<<<(unsigned)ctas, threads, smem, stream>>>(a);
+  PAM_LAUNCH_CHECK(what);
+  return PAM_OK;
+}
+
+template <int R, int STAGES, int WPC, int G>
+int launch_cd(const CdArgs& a, cudaStream_t stream) {
+  constexpr int NGROUPS = WPC / G;
+  const size_t smem = static_cast<size_t>(NGROUPS) * STAGES * (R * 32 * G * sizeof(double)) +
+                      static_cast<size_t>(NGROUPS) * STAGES * sizeof(uint64_t) +
+                      static_cast<size_t>(NGROUPS) * (2 * G + 1) * sizeof(double) +
+                      static_cast<size_t>(NGROUPS) * 96 * sizeof(double);
+  return launch_persistent(cd_kernel<R, STAGES, WPC, G>, a, a.S, WPC * 32, smem, stream, "cd_kernel");
+}
+
+template <int R, int STAGES, int WPC>
+int launch_cd_tile(const CdArgs& a, cudaStream_t stream) {
+  const size_t smem = static_cast<size_t>(WPC) * STAGES * R * 32 * sizeof(double) +
+                      static_cast<size_t>(WPC) * STAGES * sizeof(uint64_t) +
+                      static_cast<size_t>(WPC) * 144 * sizeof(double) + R * 32 * sizeof(double);
+  return launch_persistent(cd_tile_kernel<R, STAGES, WPC>, a, a.S, WPC * 32, smem, stream,
+                           "cd_tile_kernel");
+}
+
+template <int R, int STAGES, int WPC>
+int launch_cd_dual(const CdArgs& a, cudaStream_t stream) {
+  constexpr int SLOTH = R * 16;
+  const size_t smem = static_cast<size_t>(WPC) * STAGES * 2 * SLOTH * sizeof(double) +
+                      static_cast<size_t>(WPC) * STAGES * sizeof(uint64_t) +
+                      static_cast<size_t>(WPC) * 144 * sizeof(double) + SLOTH * sizeof(double);
+  return launch_persistent(cd_dual_kernel<R, STAGES, WPC>, a, (a.S + 1) / 2, WPC * 32, smem, stream,
+                           "cd_dual_kernel");
 }
 
 template <int R, int STAGES, int WPC>
@@ -1548,121 +1514,33 @@ int launch_cd_pipe(const CdArgs& a, int gcap, cudaStream_t stream) {
   constexpr int SLOT = R * 32;
   const size_t per_warp = static_cast<size_t>(STAGES) * SLOT * 8 + 96 * 8 + static_cast<size_t>(gcap) * 16;
   const size_t smem = WPC * per_warp + static_cast<size_t>((WPC * STAGES + 1) & ~1) * 8 + SLOT * 8;
-  PAM_CUDA_CHECK(cudaFuncSetAttribute(cd_pipe_kernel<R, STAGES, WPC>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int dev = 0, sms = 148;
-  PAM_CUDA_CHECK(cudaGetDevice(&dev));
-  PAM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  void* qaddr = nullptr;
-  PAM_CUDA_CHECK(cudaGetSymbolAddress(&qaddr, g_cd_queue));
-  PAM_CUDA_CHECK(cudaMemsetAsync(qaddr, 0, sizeof(unsigned), stream));
-  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(sms, ceil_div(a.S, WPC)));
-  cd_pipe_kernel<R, STAGES, WPC><<<(unsigned)ctas, WPC * 32, smem, stream>>>(a, gcap);
+  auto kernel = cd_pipe_kernel<R, STAGES, WPC>;
+  PAM_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  PAM_CUDA_CHECK(cudaMemsetAsync(a.queue, 0, sizeof(unsigned), stream));
+  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(sm_count(), ceil_div(a.S, WPC)));
+  kernel<<<(unsigned)ctas, WPC * 32, smem, stream>>>(a, gcap);
   PAM_LAUNCH_CHECK("cd_pipe_kernel");
   return PAM_OK;
 }
 
-template <int R, int STAGES, int WPC, bool CPA, int RUNS>
-int launch_cd_tile_r(const CdArgs& a, cudaStream_t stream);
-
-template <int R, int STAGES, int WPC, bool CPA = false>
-int launch_cd_tile(const CdArgs& a, cudaStream_t stream) {
-  if (tile_runs() == 1) return launch_cd_tile_r<R, STAGES, WPC, CPA, 1>(a, stream);
-  return launch_cd_tile_r<R, STAGES, WPC, CPA, 2>(a, stream);
-}
-
-template <int R, int STAGES, int WPC, bool CPA, int RUNS>
-int launch_cd_tile_r(const CdArgs& a, cudaStream_t stream) {
-  const size_t smem = static_cast<size_t>(WPC) * STAGES * R * 32 * sizeof(double) +
-                      static_cast<size_t>(WPC) * STAGES * sizeof(uint64_t) +
-                      static_cast<size_t>(WPC) * 144 * sizeof(double) + R * 32 * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    PAM_CUDA_CHECK(cudaFuncSetAttribute(cd_tile_kernel<R, STAGES, WPC, CPA, RUNS>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
+int launch_cd_large(const CdArgs& a, cudaStream_t stream) {
+  if (a.rbuf == nullptr) {
+    set_last_error("pam_cd_f64: fits above 8192 rows need the residual scratch of pam_cd_workspace_bytes");
+    return PAM_ERR_ARG;
   }
-  int dev = 0, sms = 148;
-  PAM_CUDA_CHECK(cudaGetDevice(&dev));
-  PAM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  void* qaddr = nullptr;
-  PAM_CUDA_CHECK(cudaGetSymbolAddress(&qaddr, g_cd_queue));
-  PAM_CUDA_CHECK(cudaMemsetAsync(qaddr, 0, sizeof(unsigned), stream));
-  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(sms, a.S));
-  cd_tile_kernel<R, STAGES, WPC, CPA, RUNS><<<(unsigned)ctas, WPC * 32, smem, stream>>>(a);
-  PAM_LAUNCH_CHECK("cd_tile_kernel");
+  PAM_CUDA_CHECK(cudaMemsetAsync(a.queue, 0, sizeof(unsigned), stream));
+  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(2LL * sm_count(), a.S));
+  cd_large_kernel<<<(unsigned)ctas, LG_THREADS, 0, stream>>>(a);
+  PAM_LAUNCH_CHECK("cd_large_kernel");
   return PAM_OK;
 }
 
-template <int R, int STAGES, int WPC, int RUNS>
-int launch_cd_dual(const CdArgs& a, cudaStream_t stream) {
-  constexpr int SLOTH = R * 16;
-  const size_t smem = static_cast<size_t>(WPC) * STAGES * 2 * SLOTH * sizeof(double) +
-                      static_cast<size_t>(WPC) * STAGES * sizeof(uint64_t) +
-                      static_cast<size_t>(WPC) * 144 * sizeof(double) + SLOTH * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    PAM_CUDA_CHECK(cudaFuncSetAttribute(cd_dual_kernel<R, STAGES, WPC, RUNS>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
-  int dev = 0, sms = 148;
-  PAM_CUDA_CHECK(cudaGetDevice(&dev));
-  PAM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  void* qaddr = nullptr;
-  PAM_CUDA_CHECK(cudaGetSymbolAddress(&qaddr, g_cd_queue));
-  PAM_CUDA_CHECK(cudaMemsetAsync(qaddr, 0, sizeof(unsigned), stream));
-  const int64_t pairs = (a.S + 1) / 2;
-  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(sms, pairs));
-  cd_dual_kernel<R, STAGES, WPC, RUNS><<<(unsigned)ctas, WPC * 32, smem, stream>>>(a);
-  PAM_LAUNCH_CHECK("cd_dual_kernel");
-  return PAM_OK;
-}
-
-// Two fits per warp for 257-512 rows when the batch fills >= 8 fits per SM
-// (C4: 15); below that the one-fit warps' shorter chains win.  PAM_CD_DUAL:
-// 1 forces the dual kernel, 0 disables it.
-inline bool cd_use_dual(int64_t S) {
-  const char* env = getenv("PAM_CD_DUAL");
-  if (env) return atoi(env) == 1;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return S >= 8LL * sms;
-}
-
-template <int R, int STAGES, int WPC, int G, bool TILES = false, bool KEEPW = true, bool LDGSTS = false>
-int launch_cd(const CdArgs& a, cudaStream_t stream) {
-  constexpr int NGROUPS = WPC / G;
-  const size_t smem = static_cast<size_t>(NGROUPS) * STAGES * (R * 32 * G * sizeof(double)) +
-                      static_cast<size_t>(NGROUPS) * STAGES * sizeof(uint64_t) +
-                      static_cast<size_t>(NGROUPS) * (2 * G + 1) * sizeof(double) +
-                      static_cast<size_t>(NGROUPS) * 128 * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    PAM_CUDA_CHECK(cudaFuncSetAttribute(cd_kernel<R, STAGES, WPC, G, TILES, KEEPW, LDGSTS>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
-  int dev = 0, sms = 148;
-  PAM_CUDA_CHECK(cudaGetDevice(&dev));
-  PAM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  void* qaddr = nullptr;
-  PAM_CUDA_CHECK(cudaGetSymbolAddress(&qaddr, g_cd_queue));
-  PAM_CUDA_CHECK(cudaMemsetAsync(qaddr, 0, sizeof(unsigned), stream));
-  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(sms, a.S));
-  cd_kernel<R, STAGES, WPC, G, TILES, KEEPW, LDGSTS><<<(unsigned)ctas, WPC * 32, smem, stream>>>(a);
-  PAM_LAUNCH_CHECK("cd_kernel");
-  return PAM_OK;
-}
-
+// Dense design matrices.  Many fits: one warp per fit; few fits (< 4 per SM):
+// a group of G warps per fit (shorter per-column latency); > 8192 rows: the
+// CTA-per-fit kernel with the residual in global memory.
 int cd_dispatch(const CdArgs& a, int max_rows, cudaStream_t stream) {
-  // Few subdomains relative to the SM count: spread each fit over a group of
-  // warps (shorter per-column latency); many subdomains: one warp per fit.
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const bool few = a.S < 4LL * sms;
+  if (max_rows > CD_REG_ROWS) return launch_cd_large(a, stream);
+  const bool few = a.S < 4LL * sm_count();
   if (!few || max_rows <= 64) {
     // (rows per lane, ring stages, warps per CTA): ring <= ~200 KB per CTA
     if (max_rows <= 32) return launch_cd<1, 4, 16, 1>(a, stream);
@@ -1677,44 +1555,14 @@ int cd_dispatch(const CdArgs& a, int max_rows, cudaStream_t stream) {
   if (max_rows <= 1024) return launch_cd<8, 3, 16, 4>(a, stream);
   if (max_rows <= 2048) return launch_cd<8, 3, 16, 8>(a, stream);    // 2 groups/CTA
   if (max_rows <= 4096) return launch_cd<16, 3, 8, 8>(a, stream);
-  if (max_rows <= 8192) return launch_cd<32, 3, 8, 8>(a, stream);
-  set_last_error("pam_cd_f64: subdomain has more than 8192 sample rows (kernel envelope)");
-  return PAM_ERR_UNSUPPORTED;
+  return launch_cd<32, 3, 8, 8>(a, stream);                          // <= 8192
 }
 
-__global__ void max_m_kernel(int64_t S, const int64_t* order, const int32_t* m_cur, int* out) {
-  int m = 0;
-  for (int64_t i = threadIdx.x; i < S; i += blockDim.x) m = max(m, m_cur[order ? order[i] : i]);
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  __shared__ int part[32];
-  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = max(m, part[w]);
-    *out = m;
-  }
-}
-
-// Few fits per SM (BASELINE configs 2-3, 64-256 fits): the software-pipelined
-// kernel.  PAM_CD_PIPE = 0 disables it, 1 forces it (257-1024 rows).
-int maybe_cd_pipe(const CdArgs& a, int max_rows, cudaStream_t stream, bool* used) {
-  *used = false;
-  const char* env = getenv("PAM_CD_PIPE");
-  const int mode = env ? atoi(env) : -1;
-  if (mode == 0 || max_rows <= 256 || max_rows > 1024 || tile_runs() != 1) return PAM_OK;
-  int dev = 0, sms = 148;
-  PAM_CUDA_CHECK(cudaGetDevice(&dev));
-  PAM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  if (mode != 1 && a.S > 3LL * sms) return PAM_OK;
-  // the per-warp staging holds a fit's run codes, offsets and consecutive-
-  // column products: size it from the largest dictionary of the batch
-  static int* d_m = nullptr;
-  if (!d_m) PAM_CUDA_CHECK(cudaMalloc(&d_m, sizeof(int)));
-  max_m_kernel<<<1, 1024, 0, stream>>>(a.S, a.order, a.m_cur, d_m);
-  PAM_LAUNCH_CHECK("max_m_kernel");
-  int max_m = 0;
-  PAM_CUDA_CHECK(cudaMemcpyAsync(&max_m, d_m, sizeof(int), cudaMemcpyDeviceToHost, stream));
-  PAM_CUDA_CHECK(cudaStreamSynchronize(stream));
+// Few fits per SM (BASELINE configs 2-3): the column-pair kernel; its
+// per-warp staging holds a fit's run codes, offsets and consecutive-column
+// products, sized from the largest dictionary of the batch (max_m, host).
+int launch_pair(const CdArgs& a, int max_rows, int max_m, cudaStream_t stream) {
+  const int sms = sm_count();
   const int gcap = (max_m + 31) / 32 * 32;
   const int wpc_need = static_cast<int>(std::min<int64_t>(3, std::max<int64_t>(1, ceil_div(a.S, sms))));
   // shared memory per warp: 3 slots + params + 16 B per dictionary slot
@@ -1722,9 +1570,8 @@ int maybe_cd_pipe(const CdArgs& a, int max_rows, cudaStream_t stream, bool* used
   const size_t per_warp = 3 * R * 32 * 8 + 96 * 8 + static_cast<size_t>(gcap) * 16;
   const size_t avail = 227 * 1024 - R * 32 * 8 - 64;
   const int wpc_fit = static_cast<int>(avail / per_warp);
-  if (wpc_fit < 1) return PAM_OK;  // dictionary too large for the staging
+  if (wpc_fit < 1) return PAM_ERR_UNSUPPORTED;  // dictionary too large for the staging
   const int wpc = std::min(wpc_need, wpc_fit);
-  *used = true;
   if (R == 16) {
     if (wpc >= 3) return launch_cd_pipe<16, 3, 3>(a, gcap, stream);
     if (wpc == 2) return launch_cd_pipe<16, 3, 2>(a, gcap, stream);
@@ -1735,66 +1582,82 @@ int maybe_cd_pipe(const CdArgs& a, int max_rows, cudaStream_t stream, bool* used
   return launch_cd_pipe<32, 3, 1>(a, gcap, stream);
 }
 
-int cd_dispatch_tiles(const CdArgs& a, int max_rows, cudaStream_t stream) {
-  // one warp per subdomain; tile k of a column <-> register r[k] of every lane.
-  // PAM_CD_LEAN: 1 (default) lean kernel with TMA staging; 3 lean kernel with
-  // per-lane cp.async staging; 0 the generic cd_kernel (any mask shape).  The
-  // lean kernels need masks of <= 2 runs (PAM_TILE_RUNS != 0).
-  const char* lean_env = getenv("PAM_CD_LEAN");
-  const int lean = (tile_runs() == 0) ? 0 : (lean_env ? atoi(lean_env) : 1);
-  if (lean == 1) {
-    bool used = false;
-    const int rc = maybe_cd_pipe(a, max_rows, stream, &used);
-    if (used || rc != PAM_OK) return rc;
+// Tile-packed design matrices (<= 1024 rows).  Auto selection:
+//  * 257-1024 rows and <= 3 fits per SM: the column-pair kernel;
+//  * 257-512 rows and >= 8 fits per SM (C4): two fits per warp;
+//  * otherwise one fit per warp.
+int cd_dispatch_tiles(const CdArgs& a, int max_rows, int max_m, int kernel, cudaStream_t stream) {
+  const int64_t sms = sm_count();
+  if (kernel == PAM_CD_AUTO) {
+    if (max_rows > 256 && a.S <= 3 * sms) kernel = PAM_CD_PAIR;
+    else if (max_rows > 256 && max_rows <= 512 && a.S >= 8 * sms) kernel = PAM_CD_DUAL;
+    else kernel = PAM_CD_LEAN;
   }
-  if (lean == 3 && max_rows > 32 && max_rows <= 512) {
-    if (max_rows <= 64) return launch_cd_tile<2, 4, 16, true>(a, stream);
-    if (max_rows <= 128) return launch_cd_tile<4, 4, 16, true>(a, stream);
-    if (max_rows <= 256) return launch_cd_tile<8, 4, 16, true>(a, stream);
-    return launch_cd_tile<16, 3, 16, true>(a, stream);
+  if (kernel == PAM_CD_PAIR && max_rows > 32) {
+    const int rc = launch_pair(a, max_rows, max_m, stream);
+    if (rc != PAM_ERR_UNSUPPORTED) return rc;
   }
-  if (lean == 1 || lean == 3) {
-    if (max_rows <= 32) return launch_cd_tile<1, 4, 16>(a, stream);
-    if (max_rows <= 64) return launch_cd_tile<2, 4, 16>(a, stream);
-    if (max_rows <= 128) return launch_cd_tile<4, 4, 16>(a, stream);
-    if (max_rows <= 256) return launch_cd_tile<8, 4, 16>(a, stream);
-    if (max_rows <= 512) {
-      if (max_rows > 256 && cd_use_dual(a.S)) {
-        const char* de = getenv("PAM_CD_DUAL_STAGES");  // ring-depth probe
-        if (de && atoi(de) == 2) return launch_cd_dual<32, 2, 8, 1>(a, stream);
-        if (tile_runs() == 1) return launch_cd_dual<32, 3, 8, 1>(a, stream);
-        return launch_cd_dual<32, 3, 8, 2>(a, stream);
-      }
-      const char* se = getenv("PAM_CD_STAGES");
-      if (se && atoi(se) == 4) return launch_cd_tile<16, 4, 12>(a, stream);  // deeper ring, 12 warps
-      return launch_cd_tile<16, 3, 16>(a, stream);
-    }
-    if (max_rows <= 1024) return launch_cd_tile<32, 3, 8>(a, stream);
-  }
-  if (max_rows <= 32) return launch_cd<1, 4, 16, 1, true>(a, stream);
-  if (max_rows <= 64) return launch_cd<2, 4, 16, 1, true>(a, stream);
-  if (max_rows <= 128) return launch_cd<4, 4, 16, 1, true>(a, stream);
-  if (max_rows <= 256) return launch_cd<8, 4, 16, 1, true>(a, stream);
-  if (max_rows <= 512) {
-    const char* env = getenv("PAM_CD_WPC16");
-    const int v = env ? atoi(env) : 16;
-    const char* cp = getenv("PAM_CD_COPY");
-    if (cp && cp[0] == 'l') return launch_cd<16, 3, 16, 1, true, true, true>(a, stream);
-    if (v == 24) return launch_cd<16, 2, 24, 1, true, false>(a, stream);
-    if (v == 20) return launch_cd<16, 2, 20, 1, true, false>(a, stream);
-    return launch_cd<16, 3, 16, 1, true>(a, stream);
-  }
-  if (max_rows <= 1024) return launch_cd<32, 3, 8, 1, true>(a, stream);
-  if (max_rows <= 2048) return launch_cd<64, 2, 4, 1, true>(a, stream);
-  set_last_error("pam_cd_tiles_f64: tile-packed CD supports <= 2048 rows per subdomain");
-  return PAM_ERR_UNSUPPORTED;
+  if (kernel == PAM_CD_DUAL && max_rows <= 512) return launch_cd_dual<32, 3, 8>(a, stream);
+  if (max_rows <= 32) return launch_cd_tile<1, 4, 16>(a, stream);
+  if (max_rows <= 64) return launch_cd_tile<2, 4, 16>(a, stream);
+  if (max_rows <= 128) return launch_cd_tile<4, 4, 16>(a, stream);
+  if (max_rows <= 256) return launch_cd_tile<8, 4, 16>(a, stream);
+  if (max_rows <= 512) return launch_cd_tile<16, 3, 16>(a, stream);
+  return launch_cd_tile<32, 3, 8>(a, stream);
 }
 
 }  // namespace pam
 
 using namespace pam;
 
-extern "C" int64_t pam_cd_max_rows(void) { return 8192; }
+extern "C" int64_t pam_cd_max_rows(void) { return INT32_MAX; }
+
+extern "C" int64_t pam_cd_workspace_bytes(int64_t S, int64_t total_rows, int32_t max_rows) {
+  if (S < 0 || total_rows < 0) return -1;
+  int64_t b = 256;  // work counters
+  if (max_rows > CD_REG_ROWS) b += total_rows * static_cast<int64_t>(sizeof(double));
+  return b;
+}
+
+namespace {
+CdArgs make_args(int64_t S, const int64_t* order, const int64_t* row_off, double* y,
+                 const int64_t* dict_off, const int32_t* m_cur, const int64_t* w_off, const int32_t* ld,
+                 const double* W, const double* lam1, const double* lam2, const double* tol,
+                 const int32_t* max_iters, const int32_t* active, double* beta, double* col_sq,
+                 int32_t* sweeps, int32_t* converged, double* objective, double* hist,
+                 const int64_t* hist_off, int flags, const uint64_t* tile_mask, const int64_t* col_off,
+                 const int32_t* perm, void* work) {
+  CdArgs a{};
+  a.S = S;
+  a.order = order;
+  a.row_off = row_off;
+  a.y = y;
+  a.dict_off = dict_off;
+  a.m_cur = m_cur;
+  a.w_off = w_off;
+  a.ld = ld;
+  a.W = W;
+  a.lam1 = lam1;
+  a.lam2 = lam2;
+  a.tol = tol;
+  a.max_iters = max_iters;
+  a.active = active;
+  a.beta = beta;
+  a.col_sq = col_sq;
+  a.sweeps = sweeps;
+  a.converged = converged;
+  a.objective = objective;
+  a.hist = hist;
+  a.hist_off = hist_off;
+  a.flags = flags;
+  a.tile_mask = reinterpret_cast<const unsigned long long*>(tile_mask);
+  a.col_off = col_off;
+  a.perm = perm;
+  a.queue = static_cast<unsigned*>(work);
+  a.rbuf = reinterpret_cast<double*>(static_cast<char*>(work) + 256);
+  return a;
+}
+}  // namespace
 
 extern "C" int pam_cd_ex_f64(int64_t S, const int64_t* order, const int64_t* row_off, double* y,
                              const int64_t* dict_off, const int32_t* m_cur, const int64_t* w_off,
@@ -1802,44 +1665,14 @@ extern "C" int pam_cd_ex_f64(int64_t S, const int64_t* order, const int64_t* row
                              const double* lam2, const double* tol, const int32_t* max_iters,
                              const int32_t* active, int32_t max_rows, double* beta, double* col_sq,
                              int32_t* sweeps, int32_t* converged, double* objective, double* hist,
-                             const int64_t* hist_off, int flags, void* stream) {
-  if (S < 0 || max_rows < 0) return PAM_ERR_ARG;
+                             const int64_t* hist_off, int flags, void* work, void* stream) {
+  if (S < 0 || max_rows < 0 || work == nullptr) return PAM_ERR_ARG;
   if (S == 0) return PAM_OK;
-  CdArgs a{S,    order,     row_off,   y,         dict_off, m_cur, w_off,    ld,
-           W,    lam1,      lam2,      tol,       max_iters, active, beta,   col_sq,
-           sweeps, converged, objective, hist,    hist_off, flags, nullptr, nullptr, nullptr};
+  CdArgs a = make_args(S, order, row_off, y, dict_off, m_cur, w_off, ld, W, lam1, lam2, tol, max_iters,
+                       active, beta, col_sq, sweeps, converged, objective, hist, hist_off, flags, nullptr,
+                       nullptr, nullptr, work);
+  if (max_rows <= CD_REG_ROWS) a.rbuf = nullptr;
   return cd_dispatch(a, max_rows, as_stream(stream));
-}
-
-int pam_cd_tiles_ring(int64_t S, const int64_t* order, const int64_t* row_off, const double* y,
-                      const int32_t* perm, const int64_t* dict_off, const int32_t* m_cur,
-                      const int64_t* w_off, const uint64_t* tile_mask, const int64_t* col_off,
-                      const double* W, const double* lam1, const double* lam2, const double* tol,
-                      const int32_t* max_iters, const int32_t* active, int32_t max_rows,
-                      double* beta, double* col_sq, int32_t* sweeps, int32_t* converged,
-                      double* objective, void* stream);
-
-extern "C" int pam_cd_tiles_f64(int64_t S, const int64_t* order, const int64_t* row_off,
-                                const double* y, const int32_t* perm, const int64_t* dict_off,
-                                const int32_t* m_cur, const int64_t* w_off,
-                                const uint64_t* tile_mask, const int64_t* col_off, const double* W,
-                                const double* lam1, const double* lam2, const double* tol,
-                                const int32_t* max_iters, const int32_t* active, int32_t max_rows,
-                                double* beta, double* col_sq, int32_t* sweeps, int32_t* converged,
-                                double* objective, double* hist, const int64_t* hist_off,
-                                void* stream) {
-  if (S < 0 || max_rows < 0 || !tile_mask || !col_off) return PAM_ERR_ARG;
-  if (S == 0) return PAM_OK;
-  const char* ring_env = getenv("PAM_CD_RING");
-  if (hist == nullptr && max_rows <= 1024 && ring_env && atoi(ring_env) == 1)
-    return pam_cd_tiles_ring(S, order, row_off, y, perm, dict_off, m_cur, w_off, tile_mask, col_off,
-                             W, lam1, lam2, tol, max_iters, active, max_rows, beta, col_sq, sweeps,
-                             converged, objective, stream);
-  CdArgs a{S,      order,     row_off,   const_cast<double*>(y), dict_off, m_cur, w_off, m_cur,
-           W,      lam1,      lam2,      tol,       max_iters, active, beta,   col_sq,
-           sweeps, converged, objective, hist,      hist_off,  0,
-           reinterpret_cast<const unsigned long long*>(tile_mask), col_off, perm};
-  return cd_dispatch_tiles(a, max_rows, as_stream(stream));
 }
 
 extern "C" int pam_cd_f64(int64_t S, const int64_t* order, const int64_t* row_off, const double* y,
@@ -1848,8 +1681,31 @@ extern "C" int pam_cd_f64(int64_t S, const int64_t* order, const int64_t* row_of
                           const double* lam2, const double* tol, const int32_t* max_iters,
                           const int32_t* active, int32_t max_rows, double* beta, double* col_sq,
                           int32_t* sweeps, int32_t* converged, double* objective, double* hist,
-                          const int64_t* hist_off, void* stream) {
+                          const int64_t* hist_off, void* work, void* stream) {
   return pam_cd_ex_f64(S, order, row_off, const_cast<double*>(y), dict_off, m_cur, w_off, ld, W,
                        lam1, lam2, tol, max_iters, active, max_rows, beta, col_sq, sweeps,
-                       converged, objective, hist, hist_off, 0, stream);
+                       converged, objective, hist, hist_off, 0, work, stream);
+}
+
+extern "C" int pam_cd_tiles_f64(int64_t S, const int64_t* order, const int64_t* row_off,
+                                const double* y, const int32_t* perm, const int64_t* dict_off,
+                                const int32_t* m_cur, const int64_t* w_off,
+                                const uint64_t* tile_mask, const int64_t* col_off, const double* W,
+                                const double* lam1, const double* lam2, const double* tol,
+                                const int32_t* max_iters, const int32_t* active, int32_t max_rows,
+                                int32_t max_m, double* beta, double* col_sq, int32_t* sweeps,
+                                int32_t* converged, double* objective, double* hist,
+                                const int64_t* hist_off, int32_t kernel, void* work, void* stream) {
+  if (S < 0 || max_rows < 0 || max_m < 0 || !tile_mask || !col_off || work == nullptr) return PAM_ERR_ARG;
+  if (kernel < PAM_CD_AUTO || kernel > PAM_CD_PAIR) return PAM_ERR_ARG;
+  if (max_rows > 1024) {
+    set_last_error("pam_cd_tiles_f64: tile-packed CD supports <= 1024 rows per subdomain");
+    return PAM_ERR_UNSUPPORTED;
+  }
+  if (S == 0) return PAM_OK;
+  CdArgs a = make_args(S, order, row_off, const_cast<double*>(y), dict_off, m_cur, w_off, m_cur, W, lam1,
+                       lam2, tol, max_iters, active, beta, col_sq, sweeps, converged, objective, hist,
+                       hist_off, 0, tile_mask, col_off, perm, work);
+  a.rbuf = nullptr;
+  return cd_dispatch_tiles(a, max_rows, max_m, kernel, as_stream(stream));
 }

@@ -174,34 +174,6 @@ __device__ __forceinline__ double exp_neg_scaled(double d2, double g, const unsi
   return (sb >= EXP_SHIFT_BITS + EXP_NMIN) ? Ts * p : 0.0;
 }
 
-// Variant R (PAM_EVAL_TAB=256): a 256-entry table replicated 16 times so a
-// warp's random table reads hit at most 2 shared-memory wavefronts (the 2048
-// table averages ~5), paid for by a degree-4 polynomial (one more DFMA).
-constexpr int XR_BITS = 8;
-constexpr int XR = 1 << XR_BITS;
-constexpr int XR_REP = 16;
-constexpr double EXR_K = 369.3299304675746;        // 256 / ln 2
-constexpr double EXR_C1 = 0.0027076061740622863;   // ln2/256
-constexpr double EXR_C2 = 3.665565596910106e-06;
-constexpr double EXR_C3 = 3.308302680541371e-09;
-constexpr double EXR_C4 = 2.239395190875157e-12;
-constexpr long long EXR_NMIN = -1022LL * XR;
-__device__ unsigned long long g_exp2_table_r[XR];
-
-__device__ __forceinline__ double exp_neg_scaled_r(double d2, double g, const unsigned long long* tab,
-                                                   int rep) {
-  const double s = fma(d2, -g, EXP_SHIFT);
-  const double nd = s - EXP_SHIFT;
-  const double f = fma(-g, d2, -nd);
-  const long long sb = __double_as_longlong(s);
-  const unsigned lo = static_cast<unsigned>(sb);
-  const unsigned long long tw = tab[((lo & (XR - 1)) * XR_REP) + rep];
-  const unsigned hi = static_cast<unsigned>(tw >> 32) + (lo << (20 - XR_BITS));
-  const double Ts = __hiloint2double(static_cast<int>(hi), static_cast<int>(static_cast<unsigned>(tw)));
-  const double p = fma(f, fma(f, fma(f, fma(f, EXR_C4, EXR_C3), EXR_C2), EXR_C1), 1.0);
-  return (sb >= EXP_SHIFT_BITS + EXR_NMIN) ? Ts * p : 0.0;
-}
-
 // the reference's exact max-shifted two-pass Shepard sum (rbf.py:152-167) for
 // one point, reading the dictionary from global memory (underflow fallback)
 template <int D>
@@ -230,7 +202,7 @@ __device__ double shepard_exact_point(const double* x, const double* centres, co
 // sorted_owner == nullptr: single-dictionary mode (LocalSurrogate.evaluate /
 // shepard_eval, rbf.py:152-192): every point belongs to dictionary 0 of
 // size single_m, log transform = single_exp.  perm == nullptr: identity.
-template <int D, int PT, bool REPL, typename IdxT>
+template <int D, int PT, typename IdxT>
 __global__ void __launch_bounds__(EVAL_WARPS * 32)
 eval_kernel(int64_t P, const double* __restrict__ pts, const IdxT* __restrict__ perm,
             const IdxT* __restrict__ sorted_owner, const IdxT* __restrict__ n_sorted,
@@ -240,15 +212,12 @@ eval_kernel(int64_t P, const double* __restrict__ pts, const IdxT* __restrict__ 
             const int32_t* __restrict__ log_flag, int single_m, int single_exp,
             double* __restrict__ out, int64_t* err, unsigned long long* queue) {
   constexpr int REC = (D + 2 + 1) & ~1;  // staged record: centre, g, beta (16-byte aligned)
-  constexpr int TAB = REPL ? XR * XR_REP : XT;
-  __shared__ unsigned long long tab[TAB];
+  __shared__ unsigned long long tab[XT];
   __shared__ __align__(16) double stage[EVAL_WARPS][32 * REC];
-  for (int i = threadIdx.x; i < TAB; i += blockDim.x)
-    tab[i] = REPL ? g_exp2_table_r[i / XR_REP] : g_exp2_table[i];
+  for (int i = threadIdx.x; i < XT; i += blockDim.x) tab[i] = g_exp2_table[i];
   __syncthreads();
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int rep = lane & (XR_REP - 1);
   double* const st = stage[warp];
   // sorted mode: only the located points were sorted (start[S]); the rest is
   // the error path (the caller raises)
@@ -297,7 +266,7 @@ eval_kernel(int64_t P, const double* __restrict__ pts, const IdxT* __restrict__ 
           double* r = st + lane * REC;
 #pragma unroll
           for (int k = 0; k < D; ++k) r[k] = centres[e * D + k];
-          r[D] = __dmul_rn(inv_two_sigma_sq(widths[e]), REPL ? EXR_K : EXP_K);
+          r[D] = __dmul_rn(inv_two_sigma_sq(widths[e]), EXP_K);
           r[D + 1] = beta[e];
         }
         __syncwarp();
@@ -320,7 +289,7 @@ eval_kernel(int64_t P, const double* __restrict__ pts, const IdxT* __restrict__ 
               const double dk = x[p][k] - rec[k];
               d2 = fma(dk, dk, d2);
             }
-            const double e = REPL ? exp_neg_scaled_r(d2, g, tab, rep) : exp_neg_scaled(d2, g, tab);
+            const double e = exp_neg_scaled(d2, g, tab);
             num[p] = fma(e, b, num[p]);
             den[p] += e;
           }
@@ -357,26 +326,26 @@ eval_kernel(int64_t P, const double* __restrict__ pts, const IdxT* __restrict__ 
   }
 }
 
-// points per lane (register blocking, env PAM_EVAL_PT = 2 | 4, default 4) and
-// exp table (env PAM_EVAL_TAB = 2048 | 256, default 2048)
-int eval_pt() {
-  static int pt = [] {
-    const char* e = getenv("PAM_EVAL_PT");
-    return (e && atoi(e) == 2) ? 2 : 4;
-  }();
-  return pt;
-}
-bool eval_repl() {
-  static bool r = [] {
-    const char* e = getenv("PAM_EVAL_TAB");
-    return e && atoi(e) == 256;
-  }();
-  return r;
+constexpr int EVAL_PT = 4;  // points per lane (register blocking; 2 measured slower)
+constexpr int MAX_DEVICES = 64;
+
+int current_device(int* dev) {
+  PAM_CUDA_CHECK(cudaGetDevice(dev));
+  if (*dev < 0 || *dev >= MAX_DEVICES) {
+    set_last_error("device ordinal beyond the library's per-device tables");
+    return PAM_ERR_ARG;
+  }
+  return PAM_OK;
 }
 
+// the 2^(j/2048) table is uploaded once per device (the __device__ symbol
+// exists per device)
 int ensure_exp2_table() {
-  static bool done = false;  // one GPU per process
-  if (done) return PAM_OK;
+  static bool done[MAX_DEVICES] = {};
+  int dev = 0;
+  const int rc = current_device(&dev);
+  if (rc != PAM_OK) return rc;
+  if (done[dev]) return PAM_OK;
   unsigned long long h[XT];
   for (int j = 0; j < XT; ++j) {
     const double t = static_cast<double>(exp2l(static_cast<long double>(j) / XT));
@@ -385,46 +354,7 @@ int ensure_exp2_table() {
     h[j] = b - (static_cast<unsigned long long>(static_cast<unsigned>(j) << 9) << 32);
   }
   PAM_CUDA_CHECK(cudaMemcpyToSymbol(g_exp2_table, h, sizeof(h)));
-  unsigned long long hr[XR];
-  for (int j = 0; j < XR; ++j) {
-    const double t = static_cast<double>(exp2l(static_cast<long double>(j) / XR));
-    unsigned long long b;
-    memcpy(&b, &t, sizeof(b));
-    hr[j] = b - (static_cast<unsigned long long>(static_cast<unsigned>(j) << (20 - XR_BITS)) << 32);
-  }
-  PAM_CUDA_CHECK(cudaMemcpyToSymbol(g_exp2_table_r, hr, sizeof(hr)));
-  done = true;
-  return PAM_OK;
-}
-
-template <int D, int PT, bool REPL, typename IdxT>
-int launch_eval_v(cudaStream_t st, int64_t P, const double* pts, const IdxT* perm,
-                  const IdxT* sorted_owner, const IdxT* n_sorted, const int64_t* dict_off, const int32_t* m_cur,
-                  const double* centres, const double* widths, const double* beta,
-                  const int32_t* log_flag, int single_m, int single_exp, double* out, int64_t* err,
-                  unsigned long long* queue) {
-  static int grid_cap = 0;
-  if (grid_cap == 0) {
-    int dev = 0, sms = 148, per_sm = 1;
-    PAM_CUDA_CHECK(cudaGetDevice(&dev));
-    PAM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    // maximum shared-memory carve-out, so the occupancy the grid is sized for
-    // is the one the SM actually grants
-    PAM_CUDA_CHECK(cudaFuncSetAttribute(eval_kernel<D, PT, REPL, IdxT>,
-                                        cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    PAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eval_kernel<D, PT, REPL, IdxT>,
-                                                                 EVAL_WARPS * 32, 0));
-    grid_cap = sms * std::max(per_sm, 1);
-  }
-  // with a queue: a persistent grid of one wave; without: one tile per warp
-  const int64_t tiles_ctas = ceil_div(P, static_cast<int64_t>(EVAL_WARPS) * 32 * PT);
-  const int64_t ctas = queue ? std::min<int64_t>(grid_cap, tiles_ctas) : tiles_ctas;
-  if (ctas > 0x7fffffffLL) return PAM_ERR_ARG;
-  if (queue) PAM_CUDA_CHECK(cudaMemsetAsync(queue, 0, sizeof(unsigned long long), st));
-  eval_kernel<D, PT, REPL, IdxT><<<(unsigned)ctas, EVAL_WARPS * 32, 0, st>>>(
-      P, pts, perm, sorted_owner, n_sorted, dict_off, m_cur, centres, widths, beta, log_flag, single_m,
-      single_exp, out, err, queue);
-  PAM_LAUNCH_CHECK("eval_kernel");
+  done[dev] = true;
   return PAM_OK;
 }
 
@@ -434,17 +364,33 @@ int launch_eval(cudaStream_t st, int64_t P, const double* pts, const IdxT* perm,
                 const double* centres, const double* widths, const double* beta,
                 const int32_t* log_flag, int single_m, int single_exp, double* out, int64_t* err,
                 unsigned long long* queue) {
-  const int rc = ensure_exp2_table();
+  int rc = ensure_exp2_table();
   if (rc != PAM_OK) return rc;
-#define PAM_EVAL_ARGS st, P, pts, perm, sorted_owner, n_sorted, dict_off, m_cur, centres, widths, beta, log_flag, \
-                      single_m, single_exp, out, err, queue
-  if (eval_pt() == 4) {
-    if (eval_repl()) return launch_eval_v<D, 4, true, IdxT>(PAM_EVAL_ARGS);
-    return launch_eval_v<D, 4, false, IdxT>(PAM_EVAL_ARGS);
+  constexpr int PT = EVAL_PT;
+  auto kernel = eval_kernel<D, PT, IdxT>;
+  static int grid_cap[MAX_DEVICES] = {};  // resident CTAs of one wave, per device
+  int dev = 0;
+  rc = current_device(&dev);
+  if (rc != PAM_OK) return rc;
+  if (grid_cap[dev] == 0) {
+    int sms = 148, per_sm = 1;
+    PAM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    // maximum shared-memory carve-out, so the occupancy the grid is sized for
+    // is the one the SM actually grants
+    PAM_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    PAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, EVAL_WARPS * 32, 0));
+    grid_cap[dev] = sms * std::max(per_sm, 1);
   }
-  if (eval_repl()) return launch_eval_v<D, 2, true, IdxT>(PAM_EVAL_ARGS);
-  return launch_eval_v<D, 2, false, IdxT>(PAM_EVAL_ARGS);
-#undef PAM_EVAL_ARGS
+  // with a queue: a persistent grid of one wave; without: one tile per warp
+  const int64_t tiles_ctas = ceil_div(P, static_cast<int64_t>(EVAL_WARPS) * 32 * PT);
+  const int64_t ctas = queue ? std::min<int64_t>(grid_cap[dev], tiles_ctas) : tiles_ctas;
+  if (ctas > 0x7fffffffLL) return PAM_ERR_ARG;
+  if (queue) PAM_CUDA_CHECK(cudaMemsetAsync(queue, 0, sizeof(unsigned long long), st));
+  kernel<<<(unsigned)ctas, EVAL_WARPS * 32, 0, st>>>(P, pts, perm, sorted_owner, n_sorted, dict_off, m_cur,
+                                                     centres, widths, beta, log_flag, single_m, single_exp,
+                                                     out, err, queue);
+  PAM_LAUNCH_CHECK("eval_kernel");
+  return PAM_OK;
 }
 
 int grid_for(int64_t n, int threads) {

@@ -128,9 +128,8 @@ struct GramArgs {
   double* beta;
   int32_t* sweeps;
   int32_t* converged;
+  unsigned* queue;  // work counter in the caller's workspace
 };
-
-__device__ unsigned int g_gram_queue;
 
 // Lean covariance-form CD.  MT: coordinates per lane (M <= 32*MT, MT even);
 // SLOT: doubles per ring slot (cps = SLOT / ldg columns per slot).
@@ -367,7 +366,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_gram_kernel(const GramArgs a) 
       }
     }
     unsigned nxt = 0;
-    if (lane == 0) nxt = atomicAdd(&g_gram_queue, 1u) + total_warps;
+    if (lane == 0) nxt = atomicAdd(a.queue, 1u) + total_warps;
     item = __shfl_sync(0xffffffffu, nxt, 0);
   }
 }
@@ -376,18 +375,13 @@ template <int MT, int STAGES, int WPC, int SLOT>
 int launch_gram_cd(const GramArgs& a, cudaStream_t stream) {
   const size_t smem = static_cast<size_t>(WPC) * STAGES * (SLOT * sizeof(double) + sizeof(uint64_t)) +
                       static_cast<size_t>(WPC) * 192 * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    PAM_CUDA_CHECK(cudaFuncSetAttribute(cd_gram_kernel<MT, STAGES, WPC, SLOT>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
+  // per device and per function; set on every launch (cheap)
+  PAM_CUDA_CHECK(cudaFuncSetAttribute(cd_gram_kernel<MT, STAGES, WPC, SLOT>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 148;
   PAM_CUDA_CHECK(cudaGetDevice(&dev));
   PAM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  void* qaddr = nullptr;
-  PAM_CUDA_CHECK(cudaGetSymbolAddress(&qaddr, g_gram_queue));
-  PAM_CUDA_CHECK(cudaMemsetAsync(qaddr, 0, sizeof(unsigned), stream));
+  PAM_CUDA_CHECK(cudaMemsetAsync(a.queue, 0, sizeof(unsigned), stream));
   const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(sms, ceil_div(a.S, 1)));
   cd_gram_kernel<MT, STAGES, WPC, SLOT><<<(unsigned)ctas, WPC * 32, smem, stream>>>(a);
   PAM_LAUNCH_CHECK("cd_gram_kernel");
@@ -426,11 +420,12 @@ extern "C" int pam_cd_gram_f64(int64_t S, const int64_t* order, const int64_t* d
                                const double* G, const double* q, const double* col_sq,
                                const double* lam1, const double* lam2, const double* tol,
                                const int32_t* max_iters, const int32_t* active, int32_t max_m,
-                               double* beta, int32_t* sweeps, int32_t* converged, void* stream) {
-  if (S < 0 || max_m < 0) return PAM_ERR_ARG;
+                               double* beta, int32_t* sweeps, int32_t* converged, void* work,
+                               void* stream) {
+  if (S < 0 || max_m < 0 || work == nullptr) return PAM_ERR_ARG;
   if (S == 0) return PAM_OK;
   GramArgs a{S, order, dict_off, m_cur, g_off, ldg, G, q, col_sq, lam1, lam2, tol, max_iters,
-             active, beta, sweeps, converged};
+             active, beta, sweeps, converged, static_cast<unsigned*>(work)};
   cudaStream_t st = as_stream(stream);
   // ldg <= SLOT is required: ldg = M_cap rounded to 16
   if (max_m <= 64) return launch_gram_cd<2, 3, 16, 512>(a, st);  // 8 columns per 4 KB copy (3 % faster than 24 warps x 2 KB)

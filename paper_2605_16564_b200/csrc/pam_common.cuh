@@ -129,16 +129,6 @@ __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem
       "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-// per-thread async copies (LDGSTS): 16 bytes global -> shared, no TMA unit
-__device__ __forceinline__ void cp_async16(void* dst_smem, const void* src_gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst_smem)), "l"(src_gmem)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -209,23 +199,7 @@ __device__ __forceinline__ void bulk_g2s_dep(uint32_t dst, const void* src, uint
       : "memory");
 }
 
-__device__ __forceinline__ void cp_async16_dep(void* dst_smem, const void* src_gmem, double dep) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n\t// dep %2" ::"r"(smem_u32(dst_smem)),
-               "l"(src_gmem), "d"(dep)
-               : "memory");
-}
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
-
-// Kept-tile runs per column of the tile-packed design matrices (tiles.cu):
-// PAM_TILE_RUNS = 1 (default, one range), 2 or 0 (exact masks).  The lean CD
-// kernels (cd.cu) need <= 2 runs; exact masks select the generic kernel.
-// Two runs stream 9% fewer bytes at C4 but cost more instructions per column
-// than they save in an issue-bound kernel.
-inline int tile_runs() {
-  const char* e = getenv("PAM_TILE_RUNS");
-  const int v = e ? atoi(e) : 1;
-  return (v >= 0 && v <= 2) ? v : 1;
-}
 
 }  // namespace pam

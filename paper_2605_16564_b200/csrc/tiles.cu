@@ -68,7 +68,6 @@ struct TileArgs {
   int64_t* col_off;               // per dictionary slot (doubles, relative to w_off)
   int64_t* packed_total;          // per subdomain: doubles stored (nullable)
   double* W;
-  int runs;                       // kept-tile runs per column (0 = exact masks)
 };
 
 // (A) row statistics + tile masks
@@ -120,30 +119,15 @@ __global__ void __launch_bounds__(TL_THREADS) tile_mask_kernel(const TileArgs a)
   }
 }
 
-// Smallest superset of mask m made of at most `runs` (1 or 2) contiguous runs
-// of set bits: fill [first, last]; for two runs leave the widest hole open.
-__device__ __forceinline__ unsigned long long run_cover(unsigned long long m, int runs) {
+// Smallest superset of mask m made of one contiguous run of set bits: the
+// tiles between a column's first and last kept tile are stored too (with
+// their exact small values), so the CD addresses a column with one base.
+__device__ __forceinline__ unsigned long long run_cover(unsigned long long m) {
   if (m == 0ull) return 0ull;
   const int t0 = __ffsll(static_cast<long long>(m)) - 1;
   const int t1 = 63 - __clzll(static_cast<long long>(m));
   const unsigned long long upto = (t1 >= 63) ? ~0ull : ((2ull << t1) - 1ull);
-  const unsigned long long span = upto & ~((1ull << t0) - 1ull);
-  if (runs < 2) return span;
-  unsigned long long holes = span & ~m;
-  unsigned long long best = 0ull;
-  int best_len = 0;
-  while (holes) {
-    const int h0 = __ffsll(static_cast<long long>(holes)) - 1;
-    const unsigned long long x = ~(holes >> h0);  // hole runs end below t1 < 64
-    const int hl = __ffsll(static_cast<long long>(x)) - 1;
-    const unsigned long long run = ((1ull << hl) - 1ull) << h0;
-    if (hl > best_len) {
-      best_len = hl;
-      best = run;
-    }
-    holes &= ~run;
-  }
-  return span & ~best;
+  return upto & ~((1ull << t0) - 1ull);
 }
 
 // (B) per-subdomain exclusive scan of 32 * popcount(mask) over the columns
@@ -156,14 +140,9 @@ __global__ void __launch_bounds__(SC_THREADS) tile_scan_kernel(const TileArgs a)
   const int64_t doff = a.dict_off[s];
   const int per = (M + SC_THREADS - 1) / SC_THREADS;
   const int lo = threadIdx.x * per, hi = min(M, lo + per);
-  // Run cover: fill the holes between a column's kept tiles so every column is
-  // at most `runs` contiguous runs of tiles (interior tiles are stored with
-  // their exact small values).  runs = 1 (default): +~12% bytes at C4 over
-  // exact masks, one base and one predicate per tile in the CD; runs = 2
-  // leaves the widest hole open (+~3%) at the cost of a second base.
-  if (a.runs > 0) {
-    for (int j = lo; j < hi; ++j) a.tile_mask[doff + j] = run_cover(a.tile_mask[doff + j], a.runs);
-  }
+  // Run cover (+~12% bytes at C4 over exact masks; one base and one
+  // predicate per tile in the CD kernels, which are issue-bound)
+  for (int j = lo; j < hi; ++j) a.tile_mask[doff + j] = run_cover(a.tile_mask[doff + j]);
   int64_t acc = 0;
   for (int j = lo; j < hi; ++j) acc += 32 * __popcll(a.tile_mask[doff + j]);
   part[threadIdx.x] = acc;
@@ -235,7 +214,7 @@ extern "C" int pam_assemble_tiles_f64(int dim, int64_t S, const int64_t* row_off
                                       double* rowmax, double* rowsum, uint64_t* tile_mask,
                                       int64_t* col_off, int64_t* packed_total,
                                       int64_t total_slots, double* W, void* stream) {
-  if (S < 0 || max_rows < 0 || dim < 1 || dim > 3 || max_rows > 2048) return PAM_ERR_ARG;
+  if (S < 0 || max_rows < 0 || dim < 1 || dim > 3 || max_rows > 1024) return PAM_ERR_ARG;
   if (S == 0 || max_rows == 0) return PAM_OK;
   cudaStream_t st = as_stream(stream);
   PAM_CUDA_CHECK(cudaMemsetAsync(tile_mask, 0, total_slots * sizeof(uint64_t), st));
@@ -244,7 +223,7 @@ extern "C" int pam_assemble_tiles_f64(int dim, int64_t S, const int64_t* row_off
     TileArgs a{row_off + s0, pts, perm, dict_off + s0, m_cur + s0, centres, widths, w_off + s0,
                active ? active + s0 : nullptr, tau, rowmax, rowsum,
                reinterpret_cast<unsigned long long*>(tile_mask), col_off,
-               packed_total ? packed_total + s0 : nullptr, W, tile_runs()};
+               packed_total ? packed_total + s0 : nullptr, W};
     dim3 grid((unsigned)ceil_div(max_rows, TL_THREADS), (unsigned)cnt);
     if (dim == 1) tile_mask_kernel<1><<<grid, TL_THREADS, 0, st>>>(a);
     else if (dim == 2) tile_mask_kernel<2><<<grid, TL_THREADS, 0, st>>>(a);

@@ -27,8 +27,9 @@ HBM layout (per chunk of subdomains):
 
 from __future__ import annotations
 
+import contextlib
 import time
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 
@@ -140,17 +141,61 @@ def dictionary_capacity(m0, k_top, m_q, m_max, max_rounds):
 # the CD.  Every row of W sums to 1, so 1e-16 is below the FP64 unit roundoff
 # (1.1e-16) of each row's mass; zeroing every entry below it moves the
 # reference's adaptive fits by ~1e-13 relative (tests/test_oracle_pins.py,
-# DESIGN.md §3).  PAM_TILE_TAU=7.9e-31 (2^-100) keeps the exactly-invisible
-# threshold, PAM_TILE_TAU=0 the dense stream.
+# DESIGN.md §3).  Dropping is used only when every fit of the batch has
+# lam1 > 0: a column whose kept part is empty then gets beta = 0 exactly as in
+# the reference (|z| <= tau * sum|r| < lam1), while an unregularised fit
+# (lam1 = 0) of such a column divides by a vanishing col_sq + lam2 and must
+# see every entry.  tile_tau = 2^-100 keeps the exactly-invisible
+# threshold, 0 the dense stream.
 DEFAULT_TILE_TAU = 1e-16
+
+CD_KERNELS = {"auto": 0, "lean": 1, "dual": 2, "pair": 3}
+
+
+@dataclass(frozen=True)
+class EngineOptions:
+    """Implementation choices of the device fit (results agree to ~1e-12).
+
+    cd_form: "auto" | "residual" | "gram" (engine.cd_form); tile_tau: tile-drop
+    threshold of the packed CD stream (0 = dense); cd_kernel: "auto" | "lean"
+    | "dual" | "pair" (pam_cd_tiles_f64 kernel selection); w_budget_gb: HBM
+    budget of one device batch (None = 60 % of free memory).
+    """
+
+    cd_form: str = "auto"
+    tile_tau: float = DEFAULT_TILE_TAU
+    cd_kernel: str = "auto"
+    w_budget_gb: float | None = None
+
+
+OPTIONS = EngineOptions()
+
+
+@contextlib.contextmanager
+def options(**kw):
+    """Temporarily override engine options: ``with options(cd_form="residual"): ...``"""
+    global OPTIONS
+    old = OPTIONS
+    if "cd_kernel" in kw and kw["cd_kernel"] not in CD_KERNELS:
+        raise ValueError(f"unknown cd_kernel {kw['cd_kernel']!r}")
+    if "cd_form" in kw and kw["cd_form"] not in ("auto", "residual", "gram"):
+        raise ValueError(f"unknown cd_form {kw['cd_form']!r}")
+    OPTIONS = replace(old, **kw)
+    try:
+        yield OPTIONS
+    finally:
+        OPTIONS = old
+
+
+def set_options(**kw):
+    """Set engine options for the rest of the process (bench.py flags)."""
+    global OPTIONS
+    OPTIONS = replace(OPTIONS, **kw)
 
 
 def tile_tau() -> float:
-    """Tile-drop threshold for the packed CD stream (env PAM_TILE_TAU; 0 = dense)."""
-    import os
-
-    v = os.environ.get("PAM_TILE_TAU")
-    return DEFAULT_TILE_TAU if v is None else float(v)
+    """Tile-drop threshold for the packed CD stream (0 = dense)."""
+    return float(OPTIONS.tile_tau)
 
 
 def rcb_permutation(points: np.ndarray, leaf: int = 32) -> np.ndarray:
@@ -205,12 +250,10 @@ def cd_form(n_rows, cap) -> str:
     SM, e.g. BASELINE config 2): the residual form is bound by one fit's
     per-column dependency chain (~0.55 us per column) while the
     covariance form's chain is ~0.12 us per coordinate, so it wins whenever
-    its M*M stream still fits the HBM time (M <= 3072).  Env PAM_CD_FORM =
-    auto | residual | gram.
+    its M*M stream still fits the HBM time (M <= 3072).  OPTIONS.cd_form
+    forces one form.
     """
-    import os
-
-    forced = os.environ.get("PAM_CD_FORM", "auto")
+    forced = OPTIONS.cd_form
     cap = np.asarray(cap, dtype=np.int64)
     cmax = int(cap.max())
     if forced == "gram" and cmax <= GRAM_WIDE_MAX_M:
@@ -269,8 +312,8 @@ class FitEngine:
         self.max_rows = int(self.n_rows.max())
         if self.max_rows > nat.lib().pam_cd_max_rows():
             raise NotImplementedError(
-                f"a subdomain has {self.max_rows} cells; the CD kernel envelope is "
-                f"{nat.lib().pam_cd_max_rows()} rows per subdomain (use a finer partition)"
+                f"a subdomain has {self.max_rows} cells; the CD kernels take at most "
+                f"{nat.lib().pam_cd_max_rows()} rows per subdomain"
             )
         self.cell_size = np.asarray(cell_size, dtype=np.float64)
         self.p = _config_arrays(configs, self.n_rows, self.dim)
@@ -290,7 +333,10 @@ class FitEngine:
             raise NotImplementedError("dictionary capacity x (max_iters + 1) >= 2^31 is outside the "
                                       "CD kernel envelope")
         self.tau = tile_tau() if tau is None else float(tau)
+        if S and not np.all(p["lam1"] > 0):
+            self.tau = 0.0  # unregularised fits see every entry (see DEFAULT_TILE_TAU)
         self.tiles = self.form == "residual" and self.tau > 0.0 and self.max_rows <= 1024
+        self.cd_kernel = CD_KERNELS[OPTIONS.cd_kernel]
         self.ld = _round16(self.n_rows) if not self.tiles else (self.n_rows + 31) // 32 * 32
         wsz = self.ld * self.cap
         self.w_off = np.concatenate([[0], np.cumsum(wsz)[:-1]]).astype(np.int64)
@@ -344,6 +390,8 @@ class FitEngine:
         self.d_qoff = nat.to_dev(np.concatenate([q1o, q2o]).reshape(-1))
         self.d_qw = nat.to_dev(np.concatenate([q1w, q2w]))
         self.err = nat.ErrorWord()
+        self.d_work = t.zeros(int(nat.lib().pam_cd_workspace_bytes(S, ntot, self.max_rows)), dtype=t.uint8,
+                              device=dev)
         if self.form == "gram":
             self.ldg = _round16(self.cap)
             gsz = self.ldg * self.cap
@@ -447,29 +495,29 @@ class FitEngine:
                     len(order), P(d_order), P(self.d_dict_off), P(self.d_m_cur), P(self.d_g_off),
                     P(self.d_ldg), P(self.d_G), P(self.d_q), P(self.d_col_sq), P(self.d_lam1),
                     P(self.d_lam2), P(self.d_tol), P(self.d_max_iters), P(self.d_active), max_m,
-                    P(self.d_beta), P(self.d_sweeps), P(self.d_conv), st), "pam_cd_gram_f64")
+                    P(self.d_beta), P(self.d_sweeps), P(self.d_conv), P(self.d_work), st), "pam_cd_gram_f64")
                 # exact objective at the final beta: residual form with zero sweeps
                 nat.check(lib.pam_cd_f64(
                     len(order), P(d_order), P(self.d_row_off), P(self.d_y), P(self.d_dict_off),
                     P(self.d_m_cur), P(self.d_w_off), P(self.d_ld), P(self.d_W), P(self.d_lam1),
                     P(self.d_lam2), P(self.d_tol), P(self.d_zero_iters), P(self.d_active),
                     self.max_rows, P(self.d_beta), P(self.d_obj_colsq), P(self.d_obj_sweeps),
-                    P(self.d_obj_conv), P(self.d_obj), None, None, st), "pam_cd_f64")
+                    P(self.d_obj_conv), P(self.d_obj), None, None, P(self.d_work), st), "pam_cd_f64")
             elif self.tiles:
                 nat.check(lib.pam_cd_tiles_f64(
                     len(order), P(d_order), P(self.d_row_off), P(self.d_y), P(self.d_perm),
                     P(self.d_dict_off), P(self.d_m_cur), P(self.d_w_off), P(self.d_tile_mask),
                     P(self.d_col_off), P(self.d_W), P(self.d_lam1), P(self.d_lam2), P(self.d_tol),
-                    P(self.d_max_iters), P(self.d_active), self.max_rows, P(self.d_beta),
-                    P(self.d_col_sq), P(self.d_sweeps), P(self.d_conv), P(self.d_obj), None, None, st),
-                    "pam_cd_tiles_f64")
+                    P(self.d_max_iters), P(self.d_active), self.max_rows, int(self.m_cur.max()),
+                    P(self.d_beta), P(self.d_col_sq), P(self.d_sweeps), P(self.d_conv), P(self.d_obj), None,
+                    None, self.cd_kernel, P(self.d_work), st), "pam_cd_tiles_f64")
             else:
                 nat.check(lib.pam_cd_f64(
                     len(order), P(d_order), P(self.d_row_off), P(self.d_y), P(self.d_dict_off),
                     P(self.d_m_cur), P(self.d_w_off), P(self.d_ld), P(self.d_W), P(self.d_lam1),
                     P(self.d_lam2), P(self.d_tol), P(self.d_max_iters), P(self.d_active), self.max_rows,
                     P(self.d_beta), P(self.d_col_sq), P(self.d_sweeps), P(self.d_conv), P(self.d_obj),
-                    None, None, st), "pam_cd_f64")
+                    None, None, P(self.d_work), st), "pam_cd_f64")
             e2.record()
             nat.check(lib.pam_residual_f64(
                 dim, S, P(self.d_row_off), P(self.d_pts), P(self.d_values), P(self.d_dict_off),
@@ -584,12 +632,9 @@ def reports_for(result: EngineResult, s: int, report_cls):
 
 
 def w_budget_bytes() -> int:
-    """HBM budget for one chunk's design matrices (env PAM_W_BUDGET_GB overrides)."""
-    import os
-
-    env = os.environ.get("PAM_W_BUDGET_GB")
-    if env:
-        return int(float(env) * 2**30)
+    """HBM budget for one chunk's design matrices (OPTIONS.w_budget_gb overrides)."""
+    if OPTIONS.w_budget_gb is not None:
+        return int(float(OPTIONS.w_budget_gb) * 2**30)
     torch = nat.torch_mod()
     free, _total = torch.cuda.mem_get_info()
     return int(free * 0.6)
@@ -672,7 +717,8 @@ def fit_packed(dim, row_off, points, values, box_lo, box_hi, configs, dict_m, ce
         r0, r1 = int(row_off[a]), int(row_off[b])
         m0, m1 = int(m_off[a]), int(m_off[b])
         # the CD row order only matters for the tile-packed stream
-        use_tiles = (cd_form(n_rows[a:b], cap[a:b]) == "residual" and tile_tau() > 0
+        lam1_pos = all(c.elastic.lam1 > 0 for c in configs[a:b])
+        use_tiles = (cd_form(n_rows[a:b], cap[a:b]) == "residual" and tile_tau() > 0 and lam1_pos
                      and int(n_rows[a:b].max()) <= 1024)
         perm = np.concatenate([rcb_permutation(points[row_off[i]:row_off[i + 1]])
                                for i in range(a, b)]) if use_tiles and b - a <= 16384 else None

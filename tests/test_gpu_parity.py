@@ -13,6 +13,7 @@ import numpy as np
 import pytest
 
 import paper_2605_16564_b200 as pam
+from paper_2605_16564_b200 import engine as E
 from paper_2605_16564_b200 import workloads
 from oracle import pam_oracle as O
 
@@ -192,7 +193,7 @@ def test_fit_parallel_constant_field(cuda):
     np.testing.assert_allclose(surrogate.evaluate(pts), 3.7, rtol=1e-6)
 
 
-def test_fit_parallel_deterministic_and_chunk_independent(cuda, monkeypatch):
+def test_fit_parallel_deterministic_and_chunk_independent(cuda):
     field = pam.box_field_2d(16, 16)
     part = pam.make_partition(field.mesh, 2, 2)
     cfg = pam.AdaptiveConfig(k_top=12, m_max=72, m_q=3, max_rounds=3, elastic=EN_2D,
@@ -200,8 +201,8 @@ def test_fit_parallel_deterministic_and_chunk_independent(cuda, monkeypatch):
     spec = pam.DictionarySpec(sigma=0.0625)
     s1, r1 = pam.fit_parallel(field, part, cfg, spec, workers=1)
     s4, _ = pam.fit_parallel(field, part, cfg, spec, workers=4)
-    monkeypatch.setenv("PAM_W_BUDGET_GB", "0.0000001")  # one subdomain per device batch
-    sc, rc = pam.fit_parallel(field, part, cfg, spec)
+    with E.options(w_budget_gb=1e-7):  # one subdomain per device batch
+        sc, rc = pam.fit_parallel(field, part, cfg, spec)
     assert rc.max_concurrent == 1
     pts = np.random.default_rng(0).random((500, 2))
     for other in (s4, sc):
@@ -214,19 +215,18 @@ def test_fit_parallel_deterministic_and_chunk_independent(cuda, monkeypatch):
 
 @pytest.mark.parametrize("tau", [2.0 ** -100, 1e-16])
 @pytest.mark.parametrize("cells", [(16, 16), (40, 40)])
-def test_tile_packed_stream_matches_dense(cuda, monkeypatch, cells, tau):
+def test_tile_packed_stream_matches_dense(cuda, cells, tau):
     """Tile-dropping (tau = 2^-100 and the default 1e-16) vs exact dense streaming:
     same decisions, beta ~1e-12."""
-    monkeypatch.setenv("PAM_CD_FORM", "residual")  # few fits would pick the covariance form
     field = pam.box_field_2d(*cells)
     part = pam.make_partition(field.mesh, 2, 2)
     cfg = pam.AdaptiveConfig(k_top=cells[0], m_max=6 * cells[0], m_q=3, max_rounds=3, elastic=EN_2D,
                              offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
     spec = pam.DictionarySpec(sigma=0.5 / cells[0])
-    monkeypatch.setenv("PAM_TILE_TAU", "0")
-    dense, rd = pam.fit_parallel(field, part, cfg, spec)
-    monkeypatch.setenv("PAM_TILE_TAU", repr(tau))
-    tiled, rt = pam.fit_parallel(field, part, cfg, spec)
+    with E.options(cd_form="residual", tile_tau=0.0):  # few fits would pick the covariance form
+        dense, rd = pam.fit_parallel(field, part, cfg, spec)
+    with E.options(cd_form="residual", tile_tau=tau):
+        tiled, rt = pam.fit_parallel(field, part, cfg, spec)
     assert rt.device["cd_bytes"] < rd.device["cd_bytes"]  # tiles were actually dropped
     for a, b in zip(dense.locals, tiled.locals):
         np.testing.assert_array_equal(a.dictionary.centers, b.dictionary.centers)
@@ -237,39 +237,41 @@ def test_tile_packed_stream_matches_dense(cuda, monkeypatch, cells, tau):
             assert abs(x.rel_l2 - y.rel_l2) <= 1e-10 * x.rel_l2
 
 
-@pytest.mark.parametrize("variant", [{"PAM_CD_RING": "1"}, {"PAM_CD_LEAN": "0", "PAM_CD_COPY": "ldgsts"},
-                                     {"PAM_CD_LEAN": "0"}, {"PAM_CD_LEAN": "3"}, {"PAM_TILE_RUNS": "2"},
-                                     {"PAM_TILE_RUNS": "0"}, {"PAM_CD_STAGES": "4"}])
-def test_cd_staging_variants_match(cuda, monkeypatch, variant):
-    """Opt-in CD variants (byte ring, LDGSTS staging, generic tile kernel, per-lane
-    cp.async staging, two-run / exact tile masks, 4-slot ring) reproduce the default
-    lean kernel."""
-    monkeypatch.setenv("PAM_CD_FORM", "residual")  # few fits would pick the covariance form
-    field = pam.box_field_2d(40, 40)
-    part = pam.make_partition(field.mesh, 2, 2)  # 400 rows: the R=16 tile kernels
+@pytest.mark.parametrize("cells,parts", [((40, 40), (2, 2)), ((60, 60), (3, 3))])
+@pytest.mark.parametrize("kernel", ["lean", "dual", "pair"])
+def test_cd_kernel_choices_match(cuda, cells, parts, kernel):
+    """Every CD kernel of pam_cd_tiles_f64 (one fit per warp, two fits per warp,
+    column pairs) against the dense residual-form stream: same dictionaries,
+    beta and objectives ~1e-12 (only dot-product rounding differs)."""
+    field = pam.box_field_2d(*cells)
+    part = pam.make_partition(field.mesh, *parts)  # 400 rows: the R=16 tile kernels
     cfg = pam.AdaptiveConfig(k_top=40, m_max=240, m_q=3, max_rounds=3, elastic=EN_2D,
                              offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
-    spec = pam.DictionarySpec(sigma=0.5 / 40)
-    base, rb = pam.fit_parallel(field, part, cfg, spec)
-    for k, v in variant.items():
-        monkeypatch.setenv(k, v)
-    other, ro = pam.fit_parallel(field, part, cfg, spec)
+    spec = pam.DictionarySpec(sigma=0.5 / cells[0])
+    with E.options(cd_form="residual", tile_tau=0.0):
+        base, rb = pam.fit_parallel(field, part, cfg, spec)
+    with E.options(cd_form="residual", cd_kernel=kernel):
+        other, ro = pam.fit_parallel(field, part, cfg, spec)
     for a, b in zip(base.locals, other.locals):
         np.testing.assert_array_equal(a.dictionary.centers, b.dictionary.centers)
         assert np.max(np.abs(a.beta - b.beta)) <= 1e-10 * max(1, np.abs(a.beta).max())
+    for ra, rb_ in zip(rb.rounds, ro.rounds):
+        for x, y in zip(ra, rb_):
+            assert (x.centers, x.added) == (y.centers, y.added)
+            assert abs(x.objective - y.objective) <= 1e-10 * abs(x.objective)
 
 
-def test_gram_form_matches_residual_form(cuda, monkeypatch):
+def test_gram_form_matches_residual_form(cuda):
     """Covariance-form CD (gram.cu) vs residual form on a lattice dictionary with refinement."""
     field = pam.box_field_2d(32, 32)
     part = pam.make_partition(field.mesh, 2, 2)
     cfg = pam.AdaptiveConfig(k_top=16, m_max=96, m_q=3, max_rounds=3, elastic=EN_2D,
                              offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
     spec = pam.DictionarySpec(sigma=1.0 / 16, lattice=8)  # M0=64, cap=160 < 0.75*N=192
-    monkeypatch.setenv("PAM_CD_FORM", "residual")
-    res, rr = pam.fit_parallel(field, part, cfg, spec)
-    monkeypatch.setenv("PAM_CD_FORM", "gram")
-    gram, rg = pam.fit_parallel(field, part, cfg, spec)
+    with E.options(cd_form="residual"):
+        res, rr = pam.fit_parallel(field, part, cfg, spec)
+    with E.options(cd_form="gram"):
+        gram, rg = pam.fit_parallel(field, part, cfg, spec)
     assert rg.device["cd_bytes"] < rr.device["cd_bytes"]
     for a, b in zip(res.locals, gram.locals):
         np.testing.assert_array_equal(a.dictionary.centers, b.dictionary.centers)
@@ -368,18 +370,18 @@ def test_sharded_fit_single_rank_device_path(cuda):
 
 
 @pytest.mark.parametrize("cells", [(20, 20), (30, 30)])
-def test_lean_kernel_small_rows_odd_columns(cuda, monkeypatch, cells):
-    """Lean CD at R=4 / R=8 with odd dictionary sizes and ragged batches == the generic kernel."""
-    monkeypatch.setenv("PAM_CD_FORM", "residual")  # few fits would pick the covariance form
+def test_lean_kernel_small_rows_odd_columns(cuda, cells):
+    """Lean CD at R=4 / R=8 with odd dictionary sizes and ragged batches == the dense kernel."""
     field = pam.box_field_2d(*cells)
     part = pam.make_partition(field.mesh, 2, 2)  # 100 / 225 rows
     cfg = pam.AdaptiveConfig(k_top=7, m_max=60, m_q=3, max_rounds=3, elastic=EN_2D,
                              offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
     spec = pam.DictionarySpec(sigma=0.5 / cells[0])
-    lean, rl = pam.fit_parallel(field, part, cfg, spec)
+    with E.options(cd_form="residual", cd_kernel="lean"):  # few fits would pick the covariance form
+        lean, rl = pam.fit_parallel(field, part, cfg, spec)
     assert any(r.centers % 2 for reps in rl.rounds for r in reps)  # odd M was exercised
-    monkeypatch.setenv("PAM_CD_LEAN", "0")
-    gen, rg = pam.fit_parallel(field, part, cfg, spec)
+    with E.options(cd_form="residual", tile_tau=0.0):
+        gen, rg = pam.fit_parallel(field, part, cfg, spec)
     for a, b in zip(gen.locals, lean.locals):
         np.testing.assert_array_equal(a.dictionary.centers, b.dictionary.centers)
         assert np.max(np.abs(a.beta - b.beta)) <= 1e-10 * max(1, np.abs(a.beta).max())
@@ -412,21 +414,20 @@ def test_config1_convergent_solver_matches_reference(cuda, golden):
 
 
 @pytest.mark.parametrize("cells,px", [((32, 32), 1), ((24, 24), 2), ((40, 30), 1)])
-def test_pipelined_few_fit_kernel_matches_lean(cuda, monkeypatch, cells, px):
+def test_pipelined_few_fit_kernel_matches_lean(cuda, cells, px):
     """The software-pipelined CD for few fits (lag-1 Gram correction, cd.cu
     cd_pipe_kernel) against the lean per-column kernel: same dictionaries,
     sweeps within one, beta and objectives ~1e-12 (only dot-product rounding
     differs)."""
-    monkeypatch.setenv("PAM_CD_FORM", "residual")  # few fits would pick the covariance form
     field = pam.box_field_2d(*cells)
     part = pam.make_partition(field.mesh, px, 1)
     cfg = pam.AdaptiveConfig(k_top=24, m_max=150, m_q=3, max_rounds=3, elastic=EN_2D,
                              offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
     spec = pam.DictionarySpec(sigma=0.5 / cells[0])
-    monkeypatch.setenv("PAM_CD_PIPE", "0")
-    lean, rl = pam.fit_parallel(field, part, cfg, spec)
-    monkeypatch.setenv("PAM_CD_PIPE", "1")
-    pipe, rp = pam.fit_parallel(field, part, cfg, spec)
+    with E.options(cd_form="residual", cd_kernel="lean"):  # few fits would pick the covariance form
+        lean, rl = pam.fit_parallel(field, part, cfg, spec)
+    with E.options(cd_form="residual", cd_kernel="pair"):
+        pipe, rp = pam.fit_parallel(field, part, cfg, spec)
     for a, b in zip(lean.locals, pipe.locals):
         np.testing.assert_array_equal(a.dictionary.centers, b.dictionary.centers)
         assert np.max(np.abs(a.beta - b.beta)) <= 1e-10 * max(1, np.abs(a.beta).max())
@@ -436,7 +437,7 @@ def test_pipelined_few_fit_kernel_matches_lean(cuda, monkeypatch, cells, px):
             assert abs(x.objective - y.objective) <= 1e-10 * abs(x.objective)
 
 
-def test_wide_gram_form_for_few_fits_matches_residual(cuda, monkeypatch):
+def test_wide_gram_form_for_few_fits_matches_residual(cuda):
     """Few fits with a wide dictionary (M > 512): the host picks the covariance
     form (gram.cu wide configurations, engine.cd_form); same dictionaries and
     reports as the residual form, beta ~1e-12."""
@@ -445,11 +446,9 @@ def test_wide_gram_form_for_few_fits_matches_residual(cuda, monkeypatch):
     cfg = pam.AdaptiveConfig(k_top=24, m_max=150, m_q=3, max_rounds=3, elastic=EN_2D,
                              offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
     spec = pam.DictionarySpec(sigma=1.0 / 32)
-    from paper_2605_16564_b200 import engine as E
     assert E.cd_form([1024], [1024 + 144]) == "gram"
-    monkeypatch.setenv("PAM_CD_FORM", "residual")
-    res, rr = pam.fit_parallel(field, part, cfg, spec)
-    monkeypatch.setenv("PAM_CD_FORM", "auto")
+    with E.options(cd_form="residual"):
+        res, rr = pam.fit_parallel(field, part, cfg, spec)
     gram, rg = pam.fit_parallel(field, part, cfg, spec)
     for a, b in zip(res.locals, gram.locals):
         np.testing.assert_array_equal(a.dictionary.centers, b.dictionary.centers)
@@ -493,24 +492,22 @@ def test_c5_device_generator(cuda):
 
 @pytest.mark.parametrize("cells,parts,tol", [((60, 60), (3, 3), 1e-6), ((48, 36), (2, 2), 1e-6),
                                              ((60, 60), (3, 3), 1e-3), ((50, 50), (5, 1), 1e-4)])
-def test_dual_fit_kernel_matches_lean(cuda, monkeypatch, cells, parts, tol):
+def test_dual_fit_kernel_matches_lean(cuda, cells, parts, tol):
     """Two fits per warp (cd.cu cd_dual_kernel, one fit per half-warp, 257-512
     rows) against the one-fit-per-warp lean kernel: odd fit counts (a lone
     half), ragged dictionaries after enrichment (padded columns), fits that
     converge at different sweeps (a finished half idles on zero columns).
     Same dictionaries, sweeps within one, beta and objectives ~1e-12."""
-    monkeypatch.setenv("PAM_CD_FORM", "residual")
-    monkeypatch.setenv("PAM_CD_PIPE", "0")
     field = pam.box_field_2d(*cells)
     part = pam.make_partition(field.mesh, *parts)
     en = pam.ElasticNetConfig(lam1=4.59e-4, lam2=1e-4, tol=tol, max_iters=1500)
     cfg = pam.AdaptiveConfig(k_top=40, m_max=240, m_q=3, max_rounds=3, elastic=en,
                              offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
     spec = pam.DictionarySpec(sigma=0.5 / cells[0])
-    monkeypatch.setenv("PAM_CD_DUAL", "0")
-    lean, rl = pam.fit_parallel(field, part, cfg, spec)
-    monkeypatch.setenv("PAM_CD_DUAL", "1")
-    dual, rd = pam.fit_parallel(field, part, cfg, spec)
+    with E.options(cd_form="residual", cd_kernel="lean"):
+        lean, rl = pam.fit_parallel(field, part, cfg, spec)
+    with E.options(cd_form="residual", cd_kernel="dual"):
+        dual, rd = pam.fit_parallel(field, part, cfg, spec)
     for a, b in zip(lean.locals, dual.locals):
         np.testing.assert_array_equal(a.dictionary.centers, b.dictionary.centers)
         assert np.max(np.abs(a.beta - b.beta)) <= 1e-10 * max(1, np.abs(a.beta).max())

@@ -22,8 +22,10 @@ def declared_symbols():
 
 def test_library_exists_and_loads():
     lib = _native.load_library()
-    assert lib.pam_abi_version() == 1
-    assert lib.pam_cd_max_rows() >= 2048
+    assert lib.pam_abi_version() == _native.ABI_VERSION == 2
+    assert lib.pam_cd_max_rows() >= 2**31 - 1  # no row envelope (elastic_net.py has none)
+    assert lib.pam_cd_workspace_bytes(10, 5000, 500) == 256
+    assert lib.pam_cd_workspace_bytes(1, 20000, 20000) == 256 + 8 * 20000
 
 
 def test_every_declared_symbol_is_exported_and_bound():
@@ -59,6 +61,12 @@ def test_no_cpu_fallback_without_gpu():
         pam.shepard_features(np.zeros((3, 1)), d)
     with pytest.raises(_native.NativeUnavailable):
         pam.fit(np.eye(2), np.ones(2), pam.ElasticNetConfig())
+
+
+def test_no_environment_switches_in_native_code():
+    """Kernel selection is explicit (C-ABI arguments / engine options), never getenv."""
+    for p in (ROOT / "paper_2605_16564_b200" / "csrc").glob("*.cu*"):
+        assert "getenv" not in p.read_text(), p
 
 
 def test_product_never_imports_oracle():
