@@ -102,6 +102,18 @@ int pam_assemble_f64(int dim, int64_t S, const int64_t* row_off, const double* p
                      const int64_t* w_off, const int32_t* ld, const int32_t* active,
                      int32_t max_rows, int mode, double* W, void* stream);
 
+/* Initial dictionaries into capacity slots (DictionarySpec.build /
+ * centroid_dictionary, partition.py:96-112, rbf.py:195-214; RbfDictionary
+ * generations default 0, rbf.py:28-60): entries src_off[s]..src_off[s+1]-1
+ * of the packed source (centres (n, dim), widths or the per-subdomain
+ * sigma[s], generations or 0) land in slots dict_off[s].. in order.  For the
+ * per-cell dictionary the source is the gathered sample points themselves
+ * (src_off = row_off). */
+int pam_dict_scatter_f64(int dim, int64_t S, const int64_t* src_off, const double* src_centres,
+                         const double* src_widths, const double* sigma, const int32_t* src_gens,
+                         const int64_t* dict_off, double* centres, double* widths, int32_t* gens,
+                         void* stream);
+
 /* Row normalisation of a row-major (N, M) feature matrix (shepard_normalize,
  * rbf.py:131-144).  mode 1: input holds exponents L -> exp(L - rowmax) /
  * rowsum.  mode 0: input holds raw values -> v / rowsum; a row whose sum is

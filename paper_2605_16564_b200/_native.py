@@ -108,6 +108,8 @@ SIGNATURES = {
         [ctypes.c_int, _ptr, _ptr, _ptr, _ptr, _ptr, _i64, _ptr, _ptr, _ptr, _ptr, _ptr],
     ),
     "pam_probe_fp64": (ctypes.c_int, [_i64, _ptr, _ptr]),
+    "pam_dict_scatter_f64": (ctypes.c_int, [ctypes.c_int, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr,
+                                            _ptr, _ptr]),
     "pam_c5_generate_f64": (ctypes.c_int, [_i64, _i32, _i32, _i32, _i32, _i32, _i32, ctypes.c_uint64, _ptr, _ptr,
                                            _ptr, _ptr]),
     "pam_p1_values_f64": (ctypes.c_int, [ctypes.c_int, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr]),
@@ -172,7 +174,7 @@ class _CountingLib:
         "pam_err_reset": 1, "pam_log_values_f64": 1, "pam_assemble_f64": 1, "pam_cd_f64": 1,
         "pam_cd_ex_f64": 1, "pam_residual_f64": 2, "pam_mark_f64": 1, "pam_enrich_f64": 1,
         "pam_locate_f64": 1, "pam_eval_f64": 5, "pam_shepard_eval_f64": 1,
-        "pam_row_normalize_f64": 1, "pam_gather_cells_f64": 1, "pam_assemble_tiles_f64": 3,
+        "pam_row_normalize_f64": 1, "pam_gather_cells_f64": 1, "pam_dict_scatter_f64": 1, "pam_assemble_tiles_f64": 3,
         "pam_cd_tiles_f64": 1, "pam_gram_f64": 2, "pam_cd_gram_f64": 1, "pam_probe_fp64": 1,
         "pam_p1_values_f64": 1, "pam_csr_spmv_f64": 1, "pam_pcg_f64": 3, "pam_c5_generate_f64": 2,  # + 5 per PCG iteration
     }

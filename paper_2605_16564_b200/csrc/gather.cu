@@ -83,6 +83,46 @@ __global__ void row_normalize_kernel(int64_t N, int64_t M, const double* __restr
 
 using namespace pam;
 
+namespace pam {
+// one thread per destination dictionary entry: subdomain s's first
+// cnt[s] = src_off[s+1]-src_off[s] slots receive entries src_off[s].. in order
+__global__ void dict_scatter_kernel(int dim, int64_t S, const int64_t* __restrict__ src_off,
+                                    const double* __restrict__ src_centres,
+                                    const double* __restrict__ src_widths,
+                                    const double* __restrict__ sigma, const int32_t* __restrict__ src_gens,
+                                    const int64_t* __restrict__ dict_off, double* __restrict__ centres,
+                                    double* __restrict__ widths, int32_t* __restrict__ gens) {
+  const int64_t total = src_off[S];
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    // owning subdomain by binary search over src_off (S+1 ascending offsets)
+    int64_t lo = 0, hi = S;
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (src_off[mid] <= g) lo = mid;
+      else hi = mid;
+    }
+    const int64_t s = lo;
+    const int64_t dst = dict_off[s] + (g - src_off[s]);
+    for (int k = 0; k < dim; ++k) centres[dst * dim + k] = src_centres[g * dim + k];
+    widths[dst] = src_widths ? src_widths[g] : sigma[s];
+    gens[dst] = src_gens ? src_gens[g] : 0;
+  }
+}
+}  // namespace pam
+
+extern "C" int pam_dict_scatter_f64(int dim, int64_t S, const int64_t* src_off, const double* src_centres,
+                                    const double* src_widths, const double* sigma, const int32_t* src_gens,
+                                    const int64_t* dict_off, double* centres, double* widths, int32_t* gens,
+                                    void* stream) {
+  if (dim < 1 || dim > 3 || S < 0 || (src_widths == nullptr && sigma == nullptr)) return PAM_ERR_ARG;
+  if (S == 0) return PAM_OK;
+  dict_scatter_kernel<<<148 * 8, 256, 0, as_stream(stream)>>>(dim, S, src_off, src_centres, src_widths, sigma,
+                                                              src_gens, dict_off, centres, widths, gens);
+  PAM_LAUNCH_CHECK("dict_scatter_kernel");
+  return PAM_OK;
+}
+
 extern "C" int pam_gather_cells_f64(int dim, const int64_t* counts, const int32_t* shape,
                                     const double* lo, const double* d, const double* values,
                                     int64_t S, const int64_t* row_off, double* pts_out,

@@ -353,8 +353,8 @@ class FitEngine:
         self.d_w_off = nat.to_dev(self.w_off)
         self.d_ld = nat.to_dev(self.ld.astype(np.int32))
         self.d_centres = t.empty(cap_tot * self.dim, dtype=f64, device=dev)
-        self.d_widths = t.ones(cap_tot, dtype=f64, device=dev)
-        self.d_gens = t.zeros(cap_tot, dtype=i32, device=dev)
+        self.d_widths = t.empty(cap_tot, dtype=f64, device=dev)
+        self.d_gens = t.empty(cap_tot, dtype=i32, device=dev)
         self.d_beta = t.zeros(cap_tot, dtype=f64, device=dev)
         self.d_col_sq = t.empty(cap_tot, dtype=f64, device=dev)
         self.d_W = t.empty(self.w_total, dtype=f64, device=dev)
@@ -412,22 +412,24 @@ class FitEngine:
             self.d_col_off = t.zeros(cap_tot, dtype=i64, device=dev)
             self.d_packed = t.zeros(S, dtype=i64, device=dev)
 
-        # ---- initial dictionary into the capacity slots
+        # ---- initial dictionary into the capacity slots (one device scatter)
         self.m_cur = m0.copy()
         if centroid_sigma is not None:
-            seg = t.repeat_interleave(t.arange(S, device=dev), t.as_tensor(self.n_rows, device=dev))
-            local = t.arange(ntot, device=dev) - self.d_row_off[seg]
-            dst = self.d_dict_off[seg] + local
-            self.d_centres.view(-1, self.dim)[dst] = pts.view(-1, self.dim)
-            self.d_widths[dst] = nat.to_dev(np.asarray(centroid_sigma, dtype=np.float64))[seg]
+            # per-cell dictionary: the gathered sample points themselves
+            d_sigma = nat.to_dev(np.asarray(centroid_sigma, dtype=np.float64))
+            nat.check(nat.lib().pam_dict_scatter_f64(
+                self.dim, S, nat.ptr(self.d_row_off), nat.ptr(pts), None, nat.ptr(d_sigma), None,
+                nat.ptr(self.d_dict_off), nat.ptr(self.d_centres), nat.ptr(self.d_widths), nat.ptr(self.d_gens),
+                nat.stream_ptr()), "pam_dict_scatter_f64")
         else:
-            seg_h = np.repeat(np.arange(S), m0)
-            local_h = np.arange(int(m0.sum())) - np.repeat(np.concatenate([[0], np.cumsum(m0)[:-1]]), m0)
-            dst = nat.to_dev(self.dict_off[seg_h] + local_h)
-            self.d_centres.view(-1, self.dim)[dst] = nat.to_dev(np.asarray(init_centres, dtype=np.float64).reshape(-1, self.dim))
-            self.d_widths[dst] = nat.to_dev(np.asarray(init_widths, dtype=np.float64))
-            if init_gens is not None:
-                self.d_gens[dst] = nat.to_dev(np.asarray(init_gens, dtype=np.int32))
+            src_off = nat.to_dev(np.concatenate([[0], np.cumsum(m0)]).astype(np.int64))
+            d_c = nat.to_dev(np.asarray(init_centres, dtype=np.float64).reshape(-1))
+            d_w = nat.to_dev(np.asarray(init_widths, dtype=np.float64))
+            d_g = None if init_gens is None else nat.to_dev(np.asarray(init_gens, dtype=np.int32))
+            nat.check(nat.lib().pam_dict_scatter_f64(
+                self.dim, S, nat.ptr(src_off), nat.ptr(d_c), nat.ptr(d_w), None, nat.ptr(d_g),
+                nat.ptr(self.d_dict_off), nat.ptr(self.d_centres), nat.ptr(self.d_widths), nat.ptr(self.d_gens),
+                nat.stream_ptr()), "pam_dict_scatter_f64")
         self.d_m_cur = nat.to_dev(self.m_cur.astype(np.int32))
 
     # ------------------------------------------------------------------

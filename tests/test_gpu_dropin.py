@@ -1,0 +1,80 @@
+"""The drop-in boundary, exercised from the REFERENCE side.
+
+1. The reference package (installed unmodified under baseline/_ref, git-ignored,
+   shipped to the GPU box) runs its OWN test files with its CD core
+   ``_cd_sweeps_jit`` (elastic_net.py:97, 113-161) and ``shepard_eval``
+   (rbf.py:152-167) swapped for the C-ABI host seams
+   ``pam_cd_sweeps_host_f64`` / ``pam_shepard_eval_host_f64`` through the
+   ctypes binding a maintainer would add (integration/fieldfit_b200.py,
+   INTEGRATION.md §2).  The suites must pass unchanged and the seams must
+   actually have been called.
+2. The paper's Table-2 experiment (acceptance criterion 5, reference
+   tests/test_acceptance.py:77-89, 202-210) through this package's public API:
+   centre counts [1024, 1636, 2248, 2860] and the reference's own dictionary,
+   coefficients and reports (golden ACC5 made by running the reference).  Its
+   round-3 fit (M = 2,860 on one subdomain) is the path that reaches the widest
+   covariance-form CD configuration (gram.cu, M <= 3072).
+"""
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2605_16564_b200 as pam
+from paper_2605_16564_b200 import engine as E
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+REF = ROOT / "baseline" / "_ref"
+REF_TESTS = REF / "tests_ref"
+
+
+@pytest.mark.parametrize("files", [
+    ("test_elastic_net.py",),
+    ("test_adaptive.py", "test_rbf.py"),
+    ("test_partition.py", "test_step_approx.py"),
+])
+def test_reference_suites_on_b200_seams(cuda, tmp_path, files):
+    if not (REF / "fieldfit").is_dir() or not REF_TESTS.is_dir():
+        pytest.skip("reference not installed under baseline/_ref (see DESIGN.md §9)")
+    counts = tmp_path / "counts.json"
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([str(REF), str(REF_TESTS), str(ROOT)]),
+               REFSEAM_COUNTS=str(counts))
+    cmd = [sys.executable, "-m", "pytest", "-q", "-p", "integration.refseam_plugin", "-p", "no:cacheprovider",
+           "--rootdir", str(REF_TESTS)] + [str(REF_TESTS / f) for f in files]
+    res = subprocess.run(cmd, cwd=str(ROOT), env=env, capture_output=True, text=True, timeout=900)
+    tail = (res.stdout + res.stderr)[-3000:]
+    assert res.returncode == 0, tail
+    assert " passed" in tail and " failed" not in tail, tail
+    calls = json.loads(counts.read_text())
+    assert calls["cd_sweeps"] + calls["shepard_eval"] > 0, calls
+    if "test_elastic_net.py" in files:
+        assert calls["cd_sweeps"] >= 10, calls  # the reference fit() really ran on the GPU seam
+    if "test_rbf.py" in files:
+        assert calls["shepard_eval"] >= 1, calls
+
+
+def test_acceptance_criterion_5_table2(cuda, golden):
+    g = golden("ACC5")
+    field = pam.box_field_2d()
+    import hashlib
+
+    assert str(g["input_digest"]) == hashlib.sha256(np.ascontiguousarray(field.values).tobytes()).hexdigest()
+    part = pam.make_partition(field.mesh, 1, 1)
+    cfg = pam.AdaptiveConfig(k_top=204, m_max=1836, eta=0.5, m_q=3, max_rounds=4,
+                             elastic=pam.ElasticNetConfig(lam1=4.59e-4, lam2=1e-4, tol=1e-6, max_iters=4000),
+                             offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
+    assert E.cd_form([1024], [2860]) == "gram"  # one fit: the covariance form up to M = 3072
+    sur, rep = pam.fit_parallel(field, part, cfg, pam.DictionarySpec(sigma=0.031))
+    rounds = rep.rounds[0]
+    assert [r.centers for r in rounds] == [1024, 1636, 2248, 2860]
+    assert rounds[0].rel_l2 / rounds[3].rel_l2 >= 10.0  # the criterion's error reduction
+    from test_gpu_parity_wide import check_subdomain  # tests/ is on sys.path (rootdir-relative import)
+
+    d = sur.locals[0].dictionary
+    check_subdomain(g, 0, d.centers, d.widths, d.generations, sur.locals[0].beta, rounds, sur.evaluate)

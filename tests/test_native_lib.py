@@ -69,6 +69,14 @@ def test_no_environment_switches_in_native_code():
         assert "getenv" not in p.read_text(), p
 
 
+def test_reference_side_binding_loads():
+    """integration/fieldfit_b200.py (the ctypes file a fieldfit maintainer adds) binds the seams."""
+    from integration import fieldfit_b200 as b
+
+    assert b._lib.pam_cd_sweeps_host_f64 is not None and b._lib.pam_shepard_eval_host_f64 is not None
+    assert callable(b.install)
+
+
 def test_product_never_imports_oracle():
     pkg = ROOT / "paper_2605_16564_b200"
     for p in pkg.rglob("*.py"):
