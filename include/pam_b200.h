@@ -78,6 +78,7 @@ int64_t pam_cd_max_rows(void);
 #define PAM_CD_LEAN 1 /* one fit per warp                                       */
 #define PAM_CD_DUAL 2 /* two fits per warp (257-512 rows)                       */
 #define PAM_CD_PAIR 3 /* column pairs, few fits per SM (33-1024 rows)           */
+#define PAM_CD_BLOCK 4 /* exact blocked CD, one 8-warp CTA per fit (<= 1024 rows) */
 
 /* err[0] = 0 (no error), err[1] = INT64_MAX. Device pointer. */
 int pam_err_reset(int64_t* err, void* stream);
@@ -154,11 +155,13 @@ int pam_c5_generate_f64(int64_t n_sub, int32_t n_pts, int32_t lx, int32_t ly, in
  * solution on exit.  Outputs per subdomain: sweeps, converged, objective
  * (= history[sweeps-1]).  hist/hist_off may be NULL; otherwise the per-sweep
  * objective of subdomain s is written to hist[hist_off[s] + sweep].
- * `work`: device workspace of pam_cd_workspace_bytes(S, sum N_s, max_rows)
- * bytes (work counter; residual scratch for fits above 8192 rows).  Fits of
- * up to 8192 rows keep the residual in registers (one warp, or a group of
- * 4-8 warps when there are fewer than 4 fits per SM). */
-int64_t pam_cd_workspace_bytes(int64_t S, int64_t total_rows, int32_t max_rows);
+ * `work`: device workspace of pam_cd_workspace_bytes(S, sum N_s, total
+ * dictionary slots, max_rows, kernel) bytes (work counter; residual scratch
+ * for fits above 8192 rows; block descriptors and diagonal Gram blocks for
+ * PAM_CD_BLOCK).  Fits of up to 8192 rows keep the residual in registers (one
+ * warp, or a group of 4-8 warps when there are fewer than 4 fits per SM). */
+int64_t pam_cd_workspace_bytes(int64_t S, int64_t total_rows, int64_t total_slots, int32_t max_rows,
+                               int32_t kernel);
 int pam_cd_f64(int64_t S, const int64_t* order, const int64_t* row_off, const double* y,
                const int64_t* dict_off, const int32_t* m_cur, const int64_t* w_off,
                const int32_t* ld, const double* W, const double* lam1, const double* lam2,
@@ -192,10 +195,13 @@ int pam_cd_ex_f64(int64_t S, const int64_t* order, const int64_t* row_off, doubl
  * pam_cd_tiles_f64 is pam_cd_f64 over that layout: one cp.async.bulk of
  * popcount(mask)*256 bytes per column; y is read through perm; max_m = the
  * largest m_cur of the batch (host-known; sizes the few-fit kernel's
- * staging).  kernel = PAM_CD_AUTO: 257-1024-row fits with <= 3 fits per SM
- * run the column-pair kernel, 257-512-row fits with >= 8 fits per SM two
- * fits per warp, everything else one fit per warp; results are the same
- * either way up to dot-product rounding.  `work` as for pam_cd_f64. */
+ * staging).  kernel = PAM_CD_AUTO: 257-1024-row fits with <= 1 fit per SM
+ * run the exact blocked CD (a CTA per fit: block dots, in-block updates
+ * through the diagonal Gram block, one block AXPY), with <= 3 fits per SM the
+ * column-pair kernel, 257-512-row fits with
+ * >= 8 fits per SM two fits per warp, everything else one fit per warp;
+ * results are the same either way up to dot-product rounding.  `work` as for
+ * pam_cd_f64 (sized with the same `kernel`). */
 int pam_assemble_tiles_f64(int dim, int64_t S, const int64_t* row_off, const double* pts,
                            const int32_t* perm, const int64_t* dict_off, const int32_t* m_cur,
                            const double* centres, const double* widths, const int64_t* w_off,

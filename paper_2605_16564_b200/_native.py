@@ -50,7 +50,7 @@ SIGNATURES = {
         [ctypes.c_int, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _i32, ctypes.c_int,
          _ptr, _ptr],
     ),
-    "pam_cd_workspace_bytes": (_i64, [_i64, _i64, _i32]),
+    "pam_cd_workspace_bytes": (_i64, [_i64, _i64, _i64, _i32, _i32]),
     "pam_cd_f64": (
         ctypes.c_int,
         [_i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _i32,

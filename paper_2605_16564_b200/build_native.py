@@ -21,8 +21,8 @@ LIB_NAME = "libpam_b200.so"
 LIB_PATH = PKG_DIR / LIB_NAME
 OBJ_DIR = PKG_DIR / "build"
 
-SOURCES = ["assemble.cu", "tiles.cu", "cd.cu", "gram.cu", "residual.cu", "evaluate.cu", "gather.cu", "darcy.cu", "capi.cu"]
-HEADERS = ["pam_common.cuh", "shepard.cuh"]
+SOURCES = ["assemble.cu", "tiles.cu", "cd.cu", "cd_block.cu", "gram.cu", "residual.cu", "evaluate.cu", "gather.cu", "darcy.cu", "capi.cu"]
+HEADERS = ["pam_common.cuh", "shepard.cuh", "cd_common.cuh"]
 
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [

@@ -91,7 +91,7 @@ extern "C" int pam_cd_sweeps_host_f64(const double* W_fortran, int64_t n, int64_
     return PAM_ERR_ARG;
   if (n > pam_cd_max_rows()) return PAM_ERR_UNSUPPORTED;
   const int64_t ld = (n + 15) / 16 * 16;
-  const int64_t wsb = pam_cd_workspace_bytes(1, n, static_cast<int32_t>(std::min<int64_t>(n, INT32_MAX)));
+  const int64_t wsb = pam_cd_workspace_bytes(1, n, m, static_cast<int32_t>(std::min<int64_t>(n, INT32_MAX)), 0);
   struct Meta {
     int64_t row_off[2], dict_off, w_off, hist_off;
     double lam1, lam2, tol;

@@ -23,48 +23,13 @@
 // sweep reads N*M*8 bytes: the kernel is HBM-bandwidth bound (SURVEY §8d,
 // K2b), ~2 FMA per 8 bytes.  For many fits of 257-512 rows (C4) the dual
 // kernel puts two fits in one warp, one per 16-lane half (cd_dual_kernel).
-#include "pam_common.cuh"
+#include "cd_common.cuh"
 
 #include <stdlib.h>
 
 #include <algorithm>
 
 namespace pam {
-
-constexpr int CD_REG_ROWS = 8192;  // rows a register-resident residual covers (cd_kernel, G = 8)
-
-enum : int { CD_COLSQ_GIVEN = 1, CD_R_GIVEN = 2, CD_WRITE_R = 4 };
-
-struct CdArgs {
-  int64_t S;
-  const int64_t* order;
-  const int64_t* row_off;
-  double* y;  // targets (or residual when CD_R_GIVEN); residual written back with CD_WRITE_R
-  const int64_t* dict_off;
-  const int32_t* m_cur;
-  const int64_t* w_off;
-  const int32_t* ld;
-  const double* W;
-  const double* lam1;
-  const double* lam2;
-  const double* tol;
-  const int32_t* max_iters;
-  const int32_t* active;
-  double* beta;
-  double* col_sq;
-  int32_t* sweeps;
-  int32_t* converged;
-  double* objective;
-  double* hist;
-  const int64_t* hist_off;
-  int flags;
-  // tile-packed design matrices (tiles.cu); null = dense column-major W
-  const unsigned long long* tile_mask;
-  const int64_t* col_off;
-  const int32_t* perm;  // tile mode: packed position -> local row (nullable = identity)
-  unsigned* queue;      // work counter in the caller's workspace (zeroed by the launcher)
-  double* rbuf;         // large-fit residual scratch (sum N doubles, workspace)
-};
 
 // named barrier over the G warps of one subdomain group (G > 1 only)
 __device__ __forceinline__ void group_bar(int id, int nthreads) {
@@ -392,15 +357,6 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_kernel(const CdArgs a) {
 // Measured alternatives: per-lane cp.async staging, two-run
 // masks, dense tile placement with stale-tile clears and deeper rings were
 // all slower and have been removed.
-
-// Run code of a tile mask made of one contiguous run (tiles.cu run_cover):
-// a0 | la << 8  (run = tiles [a0, a0+la))
-__device__ __forceinline__ int tile_code(unsigned long long mk) {
-  if (mk == 0ull) return 0;
-  const int a0 = __ffsll(static_cast<long long>(mk)) - 1;
-  return a0 | (__popcll(mk) << 8);
-}
-__device__ __forceinline__ int code_tiles(int code) { return (code >> 8) & 0xff; }
 
 template <int R, int STAGES, int WPC>
 __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
@@ -1462,12 +1418,6 @@ __global__ void __launch_bounds__(LG_THREADS) cd_large_kernel(const CdArgs a) {
 // is per device and per function; the call is cheap), so one process may
 // drive several GPUs.
 
-inline int sm_count() {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return sms;
-}
 
 template <typename K>
 int launch_persistent(K kernel, const CdArgs& a, int64_t units, int threads, size_t smem,
@@ -1583,16 +1533,22 @@ int launch_pair(const CdArgs& a, int max_rows, int max_m, cudaStream_t stream) {
 }
 
 // Tile-packed design matrices (<= 1024 rows).  Auto selection:
+//  * 257-1024 rows and <= 1 fit per SM: the exact blocked CD (cd_block.cu);
 //  * 257-1024 rows and <= 3 fits per SM: the column-pair kernel;
 //  * 257-512 rows and >= 8 fits per SM (C4): two fits per warp;
 //  * otherwise one fit per warp.
-int cd_dispatch_tiles(const CdArgs& a, int max_rows, int max_m, int kernel, cudaStream_t stream) {
+int cd_auto_kernel(int64_t S, int max_rows) {
   const int64_t sms = sm_count();
-  if (kernel == PAM_CD_AUTO) {
-    if (max_rows > 256 && a.S <= 3 * sms) kernel = PAM_CD_PAIR;
-    else if (max_rows > 256 && max_rows <= 512 && a.S >= 8 * sms) kernel = PAM_CD_DUAL;
-    else kernel = PAM_CD_LEAN;
-  }
+  if (max_rows > 256 && S <= sms) return PAM_CD_BLOCK;
+  if (max_rows > 256 && S <= 3 * sms) return PAM_CD_PAIR;
+  if (max_rows > 256 && max_rows <= 512 && S >= 8 * sms) return PAM_CD_DUAL;
+  return PAM_CD_LEAN;
+}
+
+int cd_dispatch_tiles(const CdArgs& a, int max_rows, int max_m, int kernel, void* block_ws,
+                      cudaStream_t stream) {
+  if (kernel == PAM_CD_AUTO) kernel = cd_auto_kernel(a.S, max_rows);
+  if (kernel == PAM_CD_BLOCK) return launch_cd_block(a, max_rows, block_ws, stream);
   if (kernel == PAM_CD_PAIR && max_rows > 32) {
     const int rc = launch_pair(a, max_rows, max_m, stream);
     if (rc != PAM_ERR_UNSUPPORTED) return rc;
@@ -1612,10 +1568,13 @@ using namespace pam;
 
 extern "C" int64_t pam_cd_max_rows(void) { return INT32_MAX; }
 
-extern "C" int64_t pam_cd_workspace_bytes(int64_t S, int64_t total_rows, int32_t max_rows) {
-  if (S < 0 || total_rows < 0) return -1;
+extern "C" int64_t pam_cd_workspace_bytes(int64_t S, int64_t total_rows, int64_t total_slots, int32_t max_rows,
+                                          int32_t kernel) {
+  if (S < 0 || total_rows < 0 || total_slots < 0) return -1;
   int64_t b = 256;  // work counters
   if (max_rows > CD_REG_ROWS) b += total_rows * static_cast<int64_t>(sizeof(double));
+  const int k = (kernel == PAM_CD_AUTO && max_rows <= 1024) ? cd_auto_kernel(S, max_rows) : kernel;
+  if (k == PAM_CD_BLOCK && max_rows <= 1024) b += cd_block_workspace_bytes(S, total_slots);
   return b;
 }
 
@@ -1697,7 +1656,7 @@ extern "C" int pam_cd_tiles_f64(int64_t S, const int64_t* order, const int64_t* 
                                 int32_t* converged, double* objective, double* hist,
                                 const int64_t* hist_off, int32_t kernel, void* work, void* stream) {
   if (S < 0 || max_rows < 0 || max_m < 0 || !tile_mask || !col_off || work == nullptr) return PAM_ERR_ARG;
-  if (kernel < PAM_CD_AUTO || kernel > PAM_CD_PAIR) return PAM_ERR_ARG;
+  if (kernel < PAM_CD_AUTO || kernel > PAM_CD_BLOCK) return PAM_ERR_ARG;
   if (max_rows > 1024) {
     set_last_error("pam_cd_tiles_f64: tile-packed CD supports <= 1024 rows per subdomain");
     return PAM_ERR_UNSUPPORTED;
@@ -1707,5 +1666,5 @@ extern "C" int pam_cd_tiles_f64(int64_t S, const int64_t* order, const int64_t* 
                        lam2, tol, max_iters, active, beta, col_sq, sweeps, converged, objective, hist,
                        hist_off, 0, tile_mask, col_off, perm, work);
   a.rbuf = nullptr;
-  return cd_dispatch_tiles(a, max_rows, max_m, kernel, as_stream(stream));
+  return cd_dispatch_tiles(a, max_rows, max_m, kernel, static_cast<char*>(work) + 256, as_stream(stream));
 }

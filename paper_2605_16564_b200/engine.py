@@ -149,7 +149,7 @@ def dictionary_capacity(m0, k_top, m_q, m_max, max_rounds):
 # threshold, 0 the dense stream.
 DEFAULT_TILE_TAU = 1e-16
 
-CD_KERNELS = {"auto": 0, "lean": 1, "dual": 2, "pair": 3}
+CD_KERNELS = {"auto": 0, "lean": 1, "dual": 2, "pair": 3, "block": 4}
 
 
 @dataclass(frozen=True)
@@ -158,7 +158,7 @@ class EngineOptions:
 
     cd_form: "auto" | "residual" | "gram" (engine.cd_form); tile_tau: tile-drop
     threshold of the packed CD stream (0 = dense); cd_kernel: "auto" | "lean"
-    | "dual" | "pair" (pam_cd_tiles_f64 kernel selection); w_budget_gb: HBM
+    | "dual" | "pair" | "block" (pam_cd_tiles_f64 kernel selection); w_budget_gb: HBM
     budget of one device batch (None = 60 % of free memory).
     """
 
@@ -241,17 +241,18 @@ def _sm_count() -> int:
     return 148
 
 
-def cd_form(n_rows, cap) -> str:
+def cd_form(n_rows, cap, tiles_ok: bool = True) -> str:
     """Which CD formulation is faster for this batch.
 
     Residual form streams N*M doubles per sweep, the covariance (Gram) form
     M*M (hard part 1).  Many fits: the form that streams fewer
     bytes (Gram needs M <= 512 and cap <= 0.75 N).  Few fits (at most one per
-    SM, e.g. BASELINE config 2): the residual form is bound by one fit's
-    per-column dependency chain (~0.55 us per column) while the
-    covariance form's chain is ~0.12 us per coordinate, so it wins whenever
-    its M*M stream still fits the HBM time (M <= 3072).  OPTIONS.cd_form
-    forces one form.
+    SM, e.g. BASELINE config 2, the Table-2 run): with the tile-packed stream
+    (``tiles_ok``: <= 1024 rows, lam1 > 0, tau > 0) the exact blocked CD
+    (cd_block.cu) wins (C2 6.7 s vs 8.3 s, Table-2 9.8 s vs 19.8 s measured);
+    otherwise the per-column chain of the dense residual kernels (~0.55 us)
+    loses to the covariance form's (~0.12 us per coordinate) whenever its M*M
+    stream still fits the HBM time (M <= 3072).  OPTIONS.cd_form forces one form.
     """
     forced = OPTIONS.cd_form
     cap = np.asarray(cap, dtype=np.int64)
@@ -262,6 +263,8 @@ def cd_form(n_rows, cap) -> str:
         return "residual"
     if cmax <= GRAM_MAX_M and np.all(cap * 4 <= np.asarray(n_rows) * 3):
         return "gram"
+    if cap.size <= _sm_count() and tiles_ok and int(np.max(n_rows)) <= 1024:
+        return "residual"
     if cap.size <= _sm_count() and cmax <= GRAM_WIDE_MAX_M:
         t_res = cmax * 0.55e-6                                   # per sweep, chain-bound
         t_gram = max(cmax * 0.12e-6, float(np.sum(cap.astype(np.float64) ** 2)) * 8 / 6.5e12)
@@ -327,7 +330,8 @@ class FitEngine:
         self.cap = dictionary_capacity(m0, p["k_top"], p["m_q"], p["m_max"], p["max_rounds"])
         self.dict_off = np.concatenate([[0], np.cumsum(self.cap)[:-1]]).astype(np.int64)
         cap_tot = int(self.cap.sum())
-        self.form = cd_form(self.n_rows, self.cap)
+        tau0 = tile_tau() if tau is None else float(tau)
+        self.form = cd_form(self.n_rows, self.cap, tiles_ok=tau0 > 0 and bool(np.all(p["lam1"] > 0)))
         # the device column stream (prologue + sweeps) is counted in 32 bits
         if np.any(self.cap * (1 + p["max_iters"]) >= 2**31):
             raise NotImplementedError("dictionary capacity x (max_iters + 1) >= 2^31 is outside the "
@@ -390,8 +394,8 @@ class FitEngine:
         self.d_qoff = nat.to_dev(np.concatenate([q1o, q2o]).reshape(-1))
         self.d_qw = nat.to_dev(np.concatenate([q1w, q2w]))
         self.err = nat.ErrorWord()
-        self.d_work = t.zeros(int(nat.lib().pam_cd_workspace_bytes(S, ntot, self.max_rows)), dtype=t.uint8,
-                              device=dev)
+        self.d_work = t.zeros(int(nat.lib().pam_cd_workspace_bytes(
+            S, ntot, cap_tot, self.max_rows, self.cd_kernel if self.tiles else 0)), dtype=t.uint8, device=dev)
         if self.form == "gram":
             self.ldg = _round16(self.cap)
             gsz = self.ldg * self.cap
@@ -720,7 +724,8 @@ def fit_packed(dim, row_off, points, values, box_lo, box_hi, configs, dict_m, ce
         m0, m1 = int(m_off[a]), int(m_off[b])
         # the CD row order only matters for the tile-packed stream
         lam1_pos = all(c.elastic.lam1 > 0 for c in configs[a:b])
-        use_tiles = (cd_form(n_rows[a:b], cap[a:b]) == "residual" and tile_tau() > 0 and lam1_pos
+        use_tiles = (cd_form(n_rows[a:b], cap[a:b], tile_tau() > 0 and lam1_pos) == "residual"
+                     and tile_tau() > 0 and lam1_pos
                      and int(n_rows[a:b].max()) <= 1024)
         perm = np.concatenate([rcb_permutation(points[row_off[i]:row_off[i + 1]])
                                for i in range(a, b)]) if use_tiles and b - a <= 16384 else None

@@ -536,6 +536,8 @@ def _fit_range(data, partition, cfgs, specs, lo, hi):
             raise RuntimeError(f"fit failed on subdomain {a + exc.subdomain}: {exc.exc}") from exc.exc
         for k, v in res.kernel_seconds.items():
             dstats["kernel_seconds"][k] = dstats["kernel_seconds"].get(k, 0.0) + v
+        dstats["cd_form"] = eng.form
+        dstats["cd_tiles"] = bool(eng.tiles)
         nr = n_rows[a:b]
         for rec in res.rounds:
             ran = rec.ran.astype(bool)

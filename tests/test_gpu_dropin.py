@@ -59,7 +59,10 @@ def test_reference_suites_on_b200_seams(cuda, tmp_path, files):
         assert calls["shepard_eval"] >= 1, calls
 
 
-def test_acceptance_criterion_5_table2(cuda, golden):
+@pytest.mark.parametrize("form", ["auto", "gram"])
+def test_acceptance_criterion_5_table2(cuda, golden, form):
+    """auto: one fit of <= 1024 rows runs the exact blocked CD (cd_block.cu);
+    gram: the covariance form's widest configuration (gram.cu, M <= 3072)."""
     g = golden("ACC5")
     field = pam.box_field_2d()
     import hashlib
@@ -69,8 +72,10 @@ def test_acceptance_criterion_5_table2(cuda, golden):
     cfg = pam.AdaptiveConfig(k_top=204, m_max=1836, eta=0.5, m_q=3, max_rounds=4,
                              elastic=pam.ElasticNetConfig(lam1=4.59e-4, lam2=1e-4, tol=1e-6, max_iters=4000),
                              offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
-    assert E.cd_form([1024], [2860]) == "gram"  # one fit: the covariance form up to M = 3072
-    sur, rep = pam.fit_parallel(field, part, cfg, pam.DictionarySpec(sigma=0.031))
+    assert E.cd_form([1024], [2860]) == "residual"  # one fit: the blocked residual-form CD
+    with E.options(cd_form=form):
+        sur, rep = pam.fit_parallel(field, part, cfg, pam.DictionarySpec(sigma=0.031))
+    assert rep.device["cd_form"] == ("gram" if form == "gram" else "residual")
     rounds = rep.rounds[0]
     assert [r.centers for r in rounds] == [1024, 1636, 2248, 2860]
     assert rounds[0].rel_l2 / rounds[3].rel_l2 >= 10.0  # the criterion's error reduction

@@ -238,7 +238,7 @@ def test_tile_packed_stream_matches_dense(cuda, cells, tau):
 
 
 @pytest.mark.parametrize("cells,parts", [((40, 40), (2, 2)), ((60, 60), (3, 3))])
-@pytest.mark.parametrize("kernel", ["lean", "dual", "pair"])
+@pytest.mark.parametrize("kernel", ["lean", "dual", "pair", "block"])
 def test_cd_kernel_choices_match(cuda, cells, parts, kernel):
     """Every CD kernel of pam_cd_tiles_f64 (one fit per warp, two fits per warp,
     column pairs) against the dense residual-form stream: same dictionaries,
@@ -438,18 +438,20 @@ def test_pipelined_few_fit_kernel_matches_lean(cuda, cells, px):
 
 
 def test_wide_gram_form_for_few_fits_matches_residual(cuda):
-    """Few fits with a wide dictionary (M > 512): the host picks the covariance
-    form (gram.cu wide configurations, engine.cd_form); same dictionaries and
-    reports as the residual form, beta ~1e-12."""
+    """Few fits with a wide dictionary (M > 512) in the covariance form (gram.cu
+    wide configurations, the host's choice when the tile stream is unavailable):
+    same dictionaries and reports as the residual form, beta ~1e-12."""
     field = pam.box_field_2d(32, 32)
     part = pam.make_partition(field.mesh, 1, 1)  # 1,024 cells, per-cell dictionary
     cfg = pam.AdaptiveConfig(k_top=24, m_max=150, m_q=3, max_rounds=3, elastic=EN_2D,
                              offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
     spec = pam.DictionarySpec(sigma=1.0 / 32)
-    assert E.cd_form([1024], [1024 + 144]) == "gram"
+    assert E.cd_form([1024], [1024 + 144], tiles_ok=False) == "gram"  # dense residual would be chain-bound
+    assert E.cd_form([1024], [1024 + 144]) == "residual"  # the blocked CD wins with tiles
     with E.options(cd_form="residual"):
         res, rr = pam.fit_parallel(field, part, cfg, spec)
-    gram, rg = pam.fit_parallel(field, part, cfg, spec)
+    with E.options(cd_form="gram"):
+        gram, rg = pam.fit_parallel(field, part, cfg, spec)
     for a, b in zip(res.locals, gram.locals):
         np.testing.assert_array_equal(a.dictionary.centers, b.dictionary.centers)
         assert np.max(np.abs(a.beta - b.beta)) <= 1e-9 * max(1, np.abs(a.beta).max())

@@ -24,8 +24,9 @@ def test_library_exists_and_loads():
     lib = _native.load_library()
     assert lib.pam_abi_version() == _native.ABI_VERSION == 2
     assert lib.pam_cd_max_rows() >= 2**31 - 1  # no row envelope (elastic_net.py has none)
-    assert lib.pam_cd_workspace_bytes(10, 5000, 500) == 256
-    assert lib.pam_cd_workspace_bytes(1, 20000, 20000) == 256 + 8 * 20000
+    assert lib.pam_cd_workspace_bytes(10, 5000, 700, 500, 1) == 256
+    assert lib.pam_cd_workspace_bytes(1, 20000, 100, 20000, 0) == 256 + 8 * 20000
+    assert lib.pam_cd_workspace_bytes(4, 4000, 1000, 1000, 4) == 256 + 288 * 1000 + 32 * 4  # blocked CD
 
 
 def test_every_declared_symbol_is_exported_and_bound():

@@ -6,7 +6,7 @@ out (the call a user makes), after one warm-up run.  The CPU reference times
 for the same configs are in SURVEY.md §8d / Appendix B (C2 ~3 min, C3 ~20 min
 on 8 cores) and the bench's CPU arm (C4).
 
-    python tools/config_times.py C1 C2 C3
+    python tools/config_times.py C1 C2 C3 [--form residual|gram|auto] [--kernel block|pair|lean|auto]
 """
 
 from __future__ import annotations
@@ -25,7 +25,20 @@ def main():
     import paper_2605_16564_b200 as pam
     from paper_2605_16564_b200 import workloads
 
-    names = sys.argv[1:] or ["C1", "C2", "C3"]
+    import argparse
+
+    from paper_2605_16564_b200 import engine as E
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("names", nargs="*", default=["C1", "C2", "C3"])
+    ap.add_argument("--form", default="auto")
+    ap.add_argument("--kernel", default="auto")
+    ap.add_argument("--tau", type=float, default=None)
+    args = ap.parse_args()
+    E.set_options(cd_form=args.form, cd_kernel=args.kernel)
+    if args.tau is not None:
+        E.set_options(tile_tau=args.tau)
+    names = args.names
     makers = {"C1": workloads.config1, "C2": workloads.config2, "C3": workloads.config3,
               "C4": workloads.config4}
     for name in names:
@@ -38,7 +51,10 @@ def main():
         vals = sur.evaluate(wl.eval_points)
         t2 = time.perf_counter()
         rounds = [r.centers for r in rep.rounds[0]]
-        print(json.dumps({"config": name, "subdomains": part.n_subdomains, "cells": int(wl.field.mesh.n_cells),
+        print(json.dumps({"config": name, "form": args.form, "kernel": args.kernel,
+                          "cd_s": rep.device["kernel_seconds"]["cd"],
+                          "kernel_seconds": rep.device["kernel_seconds"],
+                          "subdomains": part.n_subdomains, "cells": int(wl.field.mesh.n_cells),
                           "fit_s": t1 - t0, "eval_points": int(len(wl.eval_points)), "eval_s": t2 - t1,
                           "fits_per_s": part.n_subdomains / (t1 - t0), "rounds_subdomain0": rounds,
                           "eval_checksum": float(np.sum(np.log(vals)))}), flush=True)
