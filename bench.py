@@ -119,56 +119,122 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU oracle (bounded sample) — the reference arm and the cpu_baseline leg
+# CPU arm: the REFERENCE itself (baseline/_ref, unmodified, numba CD) on the
+# host cores -- the reference arm and the cpu_baseline leg.  Without the
+# installed reference the bit-exact oracle port (oracle/) stands in.
 
-def _oracle_fit_one(args):
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    seed, s, n_eval = args
+REF_DIR = ROOT / "baseline" / "_ref"
+_CPU = {}
+
+
+def cpu_kind() -> str:
+    return "reference" if (REF_DIR / "fieldfit").is_dir() else "port"
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _cpu_init(kind: str, seed: int):
+    """Pool initializer: build the C4 field and the partition once per worker
+    (outside every timed region) and JIT the reference's CD core."""
+    os.environ["OMP_NUM_THREADS"] = "1"
     from oracle import pam_oracle as O
     from paper_2605_16564_b200 import workloads
 
-    wl = _oracle_fit_one.cache.get(seed)
-    if wl is None:
-        wl = workloads.config4(seed=seed, with_refined_eval=False)
-        _oracle_fit_one.cache[seed] = wl
+    wl = workloads.config4(seed=seed, with_refined_eval=False)
     mesh = wl.field.mesh
     boxes, _, _ = O.partition_boxes(mesh.counts, mesh.bounds, wl.shape)
-    b = boxes[s]
-    rows = O.subdomain_rows(mesh.centroids, b)
+    _CPU.update(kind=kind, wl=wl, boxes=boxes)
+    if kind == "reference":
+        sys.path.insert(0, str(REF_DIR))
+        import fieldfit.elastic_net as en
+
+        assert en._HAVE_NUMBA, "the reference arm must run the numba CD core (elastic_net.py:15-20, 97)"
+        W = np.abs(np.random.default_rng(0).standard_normal((8, 4)))
+        en.fit(W / W.sum(1, keepdims=True), np.ones(8), en.ElasticNetConfig(max_iters=5))  # JIT compile
+
+
+def _cpu_fit_one(args):
+    """Fit subdomain s of C4 (3 adaptive rounds) + evaluate n_eval points in its box."""
+    s, n_eval = args
+    from oracle import pam_oracle as O
+
+    wl, boxes, kind = _CPU["wl"], _CPU["boxes"], _CPU["kind"]
+    mesh = wl.field.mesh
+    lo, hi, op = boxes[s]
+    rows = O.subdomain_rows(mesh.centroids, boxes[s])
     cen = mesh.centroids[rows]
     c = wl.config
-    cfg = dict(lam1=c.elastic.lam1, lam2=c.elastic.lam2, tol=c.elastic.tol, max_iters=c.elastic.max_iters,
-               k_top=c.k_top, m_max=c.m_max, eta=c.eta, m_q=c.m_q, max_rounds=c.max_rounds, offsets=c.offsets)
-    t0 = time.perf_counter()
-    od = O.fit_adaptive(cen, wl.field.values[rows], mesh.cell_size, b[0], b[1], cen,
-                        np.full(rows.size, wl.spec.sigma), cfg)
-    t_fit = time.perf_counter() - t0
-    rng = np.random.default_rng(s)
-    pts = np.asarray(b[0]) + rng.random((n_eval, 3)) * (np.asarray(b[1]) - np.asarray(b[0]))
-    t0 = time.perf_counter()
-    O.surrogate_eval(pts, od["centers"], od["widths"], od["beta"])
-    t_eval = time.perf_counter() - t0
+    pts = np.asarray(lo) + np.random.default_rng(s).random((n_eval, 3)) * (np.asarray(hi) - np.asarray(lo))
+    if kind == "reference":
+        from fieldfit.adaptive import AdaptiveConfig as RA, fit_adaptive
+        from fieldfit.elastic_net import ElasticNetConfig as REN
+        from fieldfit.fields import SubdomainField
+        from fieldfit.geometry import Box
+        from fieldfit.rbf import RbfDictionary
+
+        e = c.elastic
+        rcfg = RA(k_top=c.k_top, m_max=c.m_max, eps_tol=c.eps_tol, eta=c.eta, m_q=c.m_q, max_rounds=c.max_rounds,
+                  offsets=c.offsets, quad_order=c.quad_order,
+                  elastic=REN(lam1=e.lam1, lam2=e.lam2, tol=e.tol, max_iters=e.max_iters))
+        sub = SubdomainField(box=Box(lo=lo, hi=hi, open_hi=op), cell_indices=rows, centroids=cen,
+                             values=wl.field.values[rows], cell_size=mesh.cell_size)
+        t0 = time.perf_counter()
+        sur, _ = fit_adaptive(sub, RbfDictionary(centers=cen, widths=np.full(rows.size, wl.spec.sigma)), rcfg)
+        t_fit = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        sur.evaluate(pts)
+        t_eval = time.perf_counter() - t0
+    else:
+        cfg = dict(lam1=c.elastic.lam1, lam2=c.elastic.lam2, tol=c.elastic.tol, max_iters=c.elastic.max_iters,
+                   k_top=c.k_top, m_max=c.m_max, eta=c.eta, m_q=c.m_q, max_rounds=c.max_rounds, offsets=c.offsets)
+        t0 = time.perf_counter()
+        od = O.fit_adaptive(cen, wl.field.values[rows], mesh.cell_size, lo, hi, cen,
+                            np.full(rows.size, wl.spec.sigma), cfg)
+        t_fit = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        O.surrogate_eval(pts, od["centers"], od["widths"], od["beta"])
+        t_eval = time.perf_counter() - t0
     return t_fit, t_eval, n_eval
 
 
-_oracle_fit_one.cache = {}
+class CpuArm:
+    """One process pool over all host cores, workers initialised once."""
 
+    def __init__(self, threads: int, seed: int = 4):
+        import multiprocessing as mp
 
-def cpu_sample(n_sub: int, n_eval: int, threads: int, seed: int = 4):
-    """Fit n_sub C4 subdomains (spread over the grid) with `threads` processes."""
-    subs = np.linspace(0, 2243, n_sub).astype(int)
-    t0 = time.perf_counter()
-    with ProcessPoolExecutor(max_workers=threads) as pool:
-        res = list(pool.map(_oracle_fit_one, [(seed, int(s), n_eval) for s in subs]))
-    wall = time.perf_counter() - t0
-    fit_core_s = sum(r[0] for r in res)
-    eval_core_s = sum(r[1] for r in res)
-    evals = sum(r[2] for r in res)
-    # throughput of `threads` cores working in parallel on this sample
-    fits_per_s = n_sub / wall
-    evals_per_s = evals / eval_core_s * threads
-    return {"fits_per_s": fits_per_s, "evals_per_s": evals_per_s, "wall_s": wall,
-            "fit_core_s_per_subdomain": fit_core_s / n_sub, "n_sub": n_sub, "n_eval": evals}
+        self.threads = threads
+        self.kind = cpu_kind()
+        self.pool = ProcessPoolExecutor(max_workers=threads, mp_context=mp.get_context("spawn"),
+                                        initializer=_cpu_init, initargs=(self.kind, seed))
+        # distinct subdomains across steps: a seeded permutation of all 2,244
+        self.order = np.random.default_rng(2244).permutation(2244)
+        self.next = 0
+        list(self.pool.map(_cpu_fit_one, [(int(s), 8) for s in self.take(threads)]))  # start + init all workers
+
+    def take(self, n):
+        out = [self.order[(self.next + k) % 2244] for k in range(n)]
+        self.next += n
+        return out
+
+    def step(self, n_sub: int, n_eval: int):
+        subs = self.take(n_sub)
+        t0 = time.perf_counter()
+        res = list(self.pool.map(_cpu_fit_one, [(int(s), n_eval) for s in subs]))
+        wall = time.perf_counter() - t0
+        return {"wall_s": wall, "n_sub": n_sub, "fit_core_s": sum(r[0] for r in res),
+                "eval_core_s": sum(r[1] for r in res), "n_eval": sum(r[2] for r in res)}
+
+    def close(self):
+        self.pool.shutdown()
 
 
 def host_threads():
@@ -185,27 +251,31 @@ def run_reference(args):
     if rank != 0:
         return 0
     threads = host_threads()
-    n_sub = max(threads, 8)
+    arm = CpuArm(threads)
     for _ in range(args.warmup):
-        cpu_sample(min(n_sub, threads), 200, threads)
-    times, fits, evs = [], [], []
-    for _ in range(args.steps):
-        r = cpu_sample(n_sub, 2000, threads)
-        times.append(r["wall_s"])
-        fits.append(r["fits_per_s"])
-        evs.append(r["evals_per_s"])
-    value = float(np.sum([n_sub for _ in times]) / np.sum(times))
-    sample = (f"{n_sub} of 2244 C4 subdomains per step (full adaptive fit, 3 rounds x <=4000 sweeps) "
-              f"+ 2000 evaluations per fitted subdomain, {threads} processes")
+        arm.step(threads, 200)
+    steps = [arm.step(threads, 2000) for _ in range(args.steps)]
+    arm.close()
+    wall = sum(r["wall_s"] for r in steps)
+    n_fit = sum(r["n_sub"] for r in steps)
+    value = n_fit / wall
+    fit_core = sum(r["fit_core_s"] for r in steps) / n_fit
+    evals = sum(r["n_eval"] for r in steps) / sum(r["eval_core_s"] for r in steps) * threads
+    distinct = min(2244, threads * (args.steps + args.warmup + 1))
+    sample = (f"{threads} C4 subdomains per step (one per core, full 3-round adaptive fit, <= 4000 sweeps "
+              f"per round) + 2000 evaluations each; {distinct} distinct subdomains over the run; "
+              f"{'the unmodified reference (baseline/_ref, numba CD)' if arm.kind == 'reference' else 'the bit-exact oracle port'}"
+              f" in {threads} processes, field built once per worker outside the timed steps")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": float(np.mean(times) * 1e3), "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
         "config": {"workload": "C4 SPE10-shaped 60x220x85, 6x22x17 subdomains, 2 refinement levels",
                    "sample": sample},
-        "evals": {"value": float(np.mean(evs)), "unit": "points/s"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "evals": {"value": evals, "unit": "points/s"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": arm.kind, "sample": sample,
+                         "cpu_model": cpu_model(), "fit_core_s_per_subdomain": fit_core},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -336,12 +406,15 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = host_threads()
-        n_cpu = max(threads, 8)
-        r = cpu_sample(n_cpu, 2000, threads)
-        cpu = {"value": r["fits_per_s"], "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{n_cpu} of 2244 C4 subdomains (full adaptive fit) + 2000 evals each, "
-                         f"{threads} processes, {r['wall_s']:.1f} s wall",
-               "evals_per_s": r["evals_per_s"]}
+        arm = CpuArm(threads)
+        r = arm.step(threads, 2000)
+        arm.close()
+        cpu = {"value": r["n_sub"] / r["wall_s"], "unit": UNIT, "cores": threads, "kind": arm.kind,
+               "sample": f"{threads} distinct C4 subdomains (full 3-round adaptive fit, one per core) + 2000 "
+                         f"evals each, {'the unmodified reference (baseline/_ref, numba)' if arm.kind == 'reference' else 'the oracle port'}, "
+                         f"{r['wall_s']:.1f} s wall",
+               "cpu_model": cpu_model(), "fit_core_s_per_subdomain": r["fit_core_s"] / r["n_sub"],
+               "evals_per_s": r["n_eval"] / r["eval_core_s"] * threads}
 
     hbm, src = peaks()
     achieved = cd_bytes / cd_s / 1e9 if cd_s > 0 else 0.0
@@ -380,18 +453,21 @@ def run_ours(args):
                      "dense_equivalent_bytes_per_launch": cd_dense / max(cd_launches, 1),
                      "tile_tau": E.tile_tau(),
                      "step_share": cd_s / elapsed if elapsed else None},
+        # FP64-pipe bound: the issued FP64 instructions per point-centre pair
+        # (15, pinned from SASS: 3 DADD + 3 DFMA distance, 2 DFMA + 1 DADD
+        # exponent reduction, 3 DFMA polynomial, 1 DMUL scale, 2 accumulations)
+        # against the measured DFMA issue rate (peak flop/s / 2).  The SURVEY 8d
+        # flop convention (E = 20 per exp, 33 flops per pair) is kept beside it.
         "eval_roofline": {"kernel": "eval_kernel (locate + owner sort + one-pass Shepard sum, table-driven FP64 exp)",
-                          "bound": "fp64", "unit": "GFLOP/s",
-                          "flops_per_pair": 3 * 3 + 4 + 20,
-                          "flop_convention": "SURVEY 8d: M_owner*(3d+4+E) per point, E=20 FP64 ops per exp",
-                          "pairs_per_step": eval_pairs,
-                          "achieved": eval_pairs * 33 / (eval_s / args.steps) / 1e9,
-                          "peak": fp64_peak / 1e9, "peak_source": "measured (pam_probe_fp64, FMA=2)",
-                          "frac": eval_pairs * 33 / (eval_s / args.steps) / fp64_peak,
-                          # issued FP64 instructions (SASS: 15 per pair) against the pipe's
-                          # instruction rate (peak flop/s / 2): the honest pipe utilisation
+                          "bound": "fp64", "unit": "FP64 instr/s",
                           "fp64_instr_per_pair": 15,
-                          "issued_pipe_frac": eval_pairs * 15 / (eval_s / args.steps) / (fp64_peak / 2)},
+                          "pairs_per_step": eval_pairs,
+                          "achieved": eval_pairs * 15 / (eval_s / args.steps),
+                          "peak": fp64_peak / 2, "peak_source": "measured (pam_probe_fp64: DFMA/s)",
+                          "frac": eval_pairs * 15 / (eval_s / args.steps) / (fp64_peak / 2),
+                          "convention": "issued FP64-pipe fraction (SASS-pinned 15 FP64 instructions per pair)",
+                          "survey_flop_frac": eval_pairs * 33 / (eval_s / args.steps) / fp64_peak,
+                          "survey_flop_convention": "M_owner*(3d+4+E) per point, E=20 (overstates: the exp issues 11)"},
         "kernel_seconds_per_step": {k: v / args.steps for k, v in kt.items()},
         "cd_rounds": [{**d, "achieved_gbs": d["bytes"] / d["seconds"] / 1e9 if d["seconds"] else None,
                        "max_over_mean_fit": d["max_fit_bytes"] / d["mean_fit_bytes"] if d["mean_fit_bytes"] else None}
@@ -442,43 +518,59 @@ def committed_traffic(kernel: str):
 
 
 def run_c5(args):
-    """BASELINE config 5 (throughput sweep) on a slab of the 64x32x32 unit-box grid.
+    """BASELINE config 5 (throughput sweep): 64 x 32 x layers unit boxes, 1000
+    samples each, a jittered M-centre lattice, planar interfaces; fit, then
+    evaluate n_eval = 1e8 * layers / 32 uniform points over the slab.
 
-    Not the driver's headline line: fits `64*32*layers` independent 3D
-    subdomains (1000 uniform samples, a jittered M-centre lattice, planar
-    interfaces) and evaluates 1e8 * layers/32 uniform points.  Device-resident
-    inputs; the Gram-form CD is selected automatically (M < N).
+    Strong scaling (the job is fixed): under N ranks, rank r fits the balanced
+    box range r (parallel.balanced_ranges) on its GPU with inputs generated on
+    the device for that range, the fitted dictionaries are allgathered over
+    NCCL (parallel.gather_device_dictionaries), and every rank evaluates its
+    share of the points with the full surrogate.  Time = max over ranks.
     """
     import torch
 
     from paper_2605_16564_b200 import _native as nat
     from paper_2605_16564_b200 import engine as E
-    from paper_2605_16564_b200 import workloads
+    from paper_2605_16564_b200 import parallel, workloads
     from paper_2605_16564_b200.geometry import build_mesh
     from paper_2605_16564_b200.partition import DeviceSurrogate, GlobalSurrogate, make_partition
 
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     layers = args.c5_layers
-    n_sub = 64 * 32 * layers
+    n_total = 64 * 32 * layers
+    a, b = parallel.balanced_ranges(np.ones(n_total), world)[rank]
+    n_sub = b - a
     n_eval = int(1e8 * layers / 32)
-    if args.c5_gen == "device":  # pam_c5_generate_f64: same distributions, counter-based stream
-        p = workloads.config5_device(M=args.m, n_sub=n_sub)
+    pa, pb = parallel.balanced_ranges(np.ones(n_eval), world)[rank]
+    if args.c5_gen == "device" or world > 1:  # pam_c5_generate_f64 for this rank's boxes
+        p = workloads.config5_device(M=args.m, n_sub=n_sub, first_box=a)
     else:
         p = workloads.config5(M=args.m, n_sub=n_sub, n_eval=0)
-    # 1e8 uniform points over the full 64x32x32 domain, restricted to the fitted slab
-    p.eval_points = np.random.default_rng(50).random((n_eval, 3)) * np.array([64.0, 32.0, float(layers)])
+    eval_all = np.random.default_rng(50).random((n_eval, 3)) * np.array([64.0, 32.0, float(layers)])
     dev = nat.device()
     d_pts = torch.from_numpy(np.ascontiguousarray(p.points).reshape(-1)).to(dev)
     d_vals = torch.from_numpy(p.values).to(dev)
-    d_eval = torch.from_numpy(p.eval_points).to(dev)
+    d_eval = torch.from_numpy(eval_all[pa:pb]).to(dev)
+    del eval_all
     part = make_partition(build_mesh(3, (64, 32, layers), ((0.0, 64.0), (0.0, 32.0), (0.0, float(layers)))),
                           64, 32, layers)
     stream = torch.cuda.current_stream()
-    # batches whose design matrices exceed the HBM budget (the full 65,536-box
-    # sweep: ~134 GB at M = 256) go through the chunked fit_packed path and the
-    # fitted dictionaries are re-packed on the device for the evaluation
+    # shards whose design matrices exceed the HBM budget (the full 65,536-box
+    # sweep on one GPU: ~134 GB at M = 256) go through the chunked fit_packed path
     cap = E.dictionary_capacity(p.dict_m, min(p.config.k_top, 1000), p.config.m_q, p.config.m_max,
                                 p.config.max_rounds)
     chunked = int(E.device_bytes(np.diff(p.row_off), cap).sum()) > E.w_budget_bytes()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
 
     def step(rec=None):
         if chunked:
@@ -487,20 +579,19 @@ def run_c5(args):
                                p.centres, p.widths, p.cell_size)
             m = np.asarray(res.m_final, dtype=np.int64)
             off = np.concatenate([[0], np.cumsum(m)[:-1]]).astype(np.int64)
-            ds = DeviceSurrogate(3, nat.to_dev(off), nat.to_dev(m.astype(np.int32)),
-                                 nat.to_dev(np.concatenate(res.centres).reshape(-1)),
-                                 nat.to_dev(np.concatenate(res.widths)), nat.to_dev(np.concatenate(res.beta)),
-                                 torch.ones(n_sub, dtype=torch.int32, device=dev))
+            parts = (nat.to_dev(off), nat.to_dev(m.astype(np.int32)), nat.to_dev(np.concatenate(res.centres).reshape(-1)),
+                     nat.to_dev(np.concatenate(res.widths)), nat.to_dev(np.concatenate(res.beta)))
             form = "gram (chunked)"
         else:
             eng = E.FitEngine(3, p.cell_size, p.row_off, d_pts, d_vals, p.box_lo, p.box_hi, [p.config] * n_sub,
                               init_centres=p.centres, init_widths=p.widths, init_m=p.dict_m)
             res = eng.run()
-            ds = DeviceSurrogate(3, eng.d_dict_off, eng.d_m_cur, eng.d_centres, eng.d_widths,
-                                 eng.d_beta, torch.ones(n_sub, dtype=torch.int32, device=dev))
+            parts = (eng.d_dict_off, eng.d_m_cur, eng.d_centres, eng.d_widths, eng.d_beta)
             eng.d_W = None
             form = eng.form
-        gs = GlobalSurrogate(partition=part, locals=tuple([None] * n_sub))
+        g = parallel.gather_device_dictionaries(*parts, 3)  # NCCL allgatherv when world > 1
+        ds = DeviceSurrogate(3, *g, torch.ones(n_total, dtype=torch.int32, device=dev))
+        gs = GlobalSurrogate(partition=part, locals=tuple([None] * n_total))
         gs.attach_device(ds)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -511,38 +602,53 @@ def run_c5(args):
 
     for _ in range(args.warmup):
         step()
-    torch.cuda.synchronize()
-    sampler = ClockSampler(0)
+    barrier()
+    sampler = ClockSampler(local)
     sampler.start()
     recs = []
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
     s0.record(stream)
     for _ in range(args.steps):
         step(recs)
     s1.record(stream)
-    torch.cuda.synchronize()
+    barrier()
     clocks = sampler.stop()
     el = s0.elapsed_time(s1) / 1e3
-    ev = sum(a.elapsed_time(b) for _, a, b, _ in recs) / 1e3
+    ev = sum(x.elapsed_time(y) for _, x, y, _ in recs) / 1e3
     cd = sum(r.kernel_seconds["cd"] for r, _, _, _ in recs)
     streamed = sum(int(np.sum(rec.stream_doubles[rec.ran] * (rec.sweeps[rec.ran].astype(np.int64) + 1)))
                    for r, _, _, _ in recs for rec in r.rounds) * 8
+    if world > 1:
+        t = torch.tensor([el, ev, cd], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        el, ev, cd = (float(x) for x in t)
+        tb = torch.tensor([float(streamed)], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(tb)
+        streamed = float(tb[0])
     sweeps = [int(np.mean(rec.sweeps)) for rec in recs[0][0].rounds]
     hbm, src = peaks()
-    print(json.dumps({
-        "metric": METRIC, "value": n_sub * args.steps / el, "unit": UNIT, "n_gpus": 1,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": f"C5 throughput sweep slab: {n_sub} unit boxes x 1000 "
-                                                    f"samples, M={args.m}, {n_eval} eval points",
-                                        "cd_form": recs[0][3], "mean_sweeps": sweeps},
-        "evals": {"value": n_eval * args.steps / ev, "unit": "points/s"},
-        "roofline": {"kernel": f"cd ({recs[0][3]} form)", "bound": "hbm", "achieved": streamed / cd / 1e9,
-                     "peak": hbm, "unit": "GB/s", "frac": streamed / cd / 1e9 / hbm, "peak_source": src},
-        "kernel_seconds_per_step": {k: sum(r.kernel_seconds[k] for r, _, _, _ in recs) / args.steps
-                                    for k in recs[0][0].kernel_seconds},
-        "clocks": clocks,
-    }), flush=True)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": n_total * args.steps / el, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded C5 generator)",
+            "config": {"workload": f"C5 throughput sweep: {n_total} unit boxes x 1000 samples, M={args.m}, "
+                                   f"{n_eval} eval points, boxes sharded over {world} rank(s)",
+                       "cd_form": recs[0][3], "mean_sweeps": sweeps, "generator": "device" if
+                       (args.c5_gen == "device" or world > 1) else "host",
+                       "parallelism": f"shard x{world} + NCCL allgatherv of the dictionaries"},
+            "evals": {"value": n_eval * args.steps / ev, "unit": "points/s"},
+            "roofline": {"kernel": f"cd ({recs[0][3]} form)", "bound": "hbm",
+                         "achieved": streamed / cd / 1e9 / world, "peak": hbm, "unit": "GB/s",
+                         "frac": streamed / cd / 1e9 / world / hbm, "peak_source": src},
+            "kernel_seconds_per_step": {k: sum(r.kernel_seconds[k] for r, _, _, _ in recs) / args.steps
+                                        for k in recs[0][0].kernel_seconds},
+            "clocks": clocks,
+        }), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
     return 0
 
 
@@ -572,9 +678,37 @@ def main():
         E.set_options(cd_kernel=args.cd_kernel)
     if args.impl == "reference":
         return run_reference(args)
+    if "WORLD_SIZE" in os.environ:
+        if int(os.environ["WORLD_SIZE"]) != args.gpus:
+            raise SystemExit(f"WORLD_SIZE={os.environ['WORLD_SIZE']} but --gpus {args.gpus}")
+    elif args.gpus > 1:
+        return spawn_ranks(args)
     if args.config == "C5":
         return run_c5(args)
     return run_ours(args)
+
+
+def _rank_main(local_rank, world, port, argv):
+    os.environ.update(RANK=str(local_rank), LOCAL_RANK=str(local_rank), WORLD_SIZE=str(world),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.argv = [sys.argv[0]] + argv
+    rc = main()
+    if rc:
+        raise SystemExit(rc)
+
+
+def spawn_ranks(args):
+    """`python bench.py --gpus N` without torchrun: one process per GPU (torch.multiprocessing),
+    rendezvous on 127.0.0.1; rank 0 prints the JSON line."""
+    import socket
+
+    import torch.multiprocessing as tmp
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    tmp.spawn(_rank_main, args=(args.gpus, port, sys.argv[1:]), nprocs=args.gpus, join=True)
+    return 0
 
 
 if __name__ == "__main__":

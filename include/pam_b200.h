@@ -134,14 +134,16 @@ int pam_gather_cells_f64(int dim, const int64_t* counts, const int32_t* shape,
                          double* vals_out, int64_t* cell_idx_out, void* stream);
 
 /* On-device generator of BASELINE config 5 inputs (the
- * distributions of workloads.config5, counter-based random stream): n_sub
- * unit boxes of the gx x gy x ... tiling (x fastest), n_pts uniform samples
+ * distributions of workloads.config5, counter-based random stream): boxes
+ * first_box .. first_box + n_sub - 1 (a rank's shard; the data of a box do
+ * not depend on the range) of the gx x gy x ... unit-box tiling (x fastest),
+ * n_pts uniform samples
  * per box with values from 1-4 planar interfaces (levels 10^U[-3,3]), and
  * the jittered lx x ly x lz centre lattice per box (M = lx*ly*lz).  DEVICE
  * outputs: points (n_sub*n_pts, 3), values (n_sub*n_pts), centres
  * (n_sub*M, 3). */
-int pam_c5_generate_f64(int64_t n_sub, int32_t n_pts, int32_t lx, int32_t ly, int32_t lz, int32_t gx,
-                        int32_t gy, uint64_t seed, double* points, double* values, double* centres,
+int pam_c5_generate_f64(int64_t first_box, int64_t n_sub, int32_t n_pts, int32_t lx, int32_t ly, int32_t lz,
+                        int32_t gx, int32_t gy, uint64_t seed, double* points, double* values, double* centres,
                         void* stream);
 
 /* ---- K2b: batched cyclic coordinate descent -------------------------------

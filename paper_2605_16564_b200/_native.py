@@ -110,8 +110,8 @@ SIGNATURES = {
     "pam_probe_fp64": (ctypes.c_int, [_i64, _ptr, _ptr]),
     "pam_dict_scatter_f64": (ctypes.c_int, [ctypes.c_int, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr,
                                             _ptr, _ptr]),
-    "pam_c5_generate_f64": (ctypes.c_int, [_i64, _i32, _i32, _i32, _i32, _i32, _i32, ctypes.c_uint64, _ptr, _ptr,
-                                           _ptr, _ptr]),
+    "pam_c5_generate_f64": (ctypes.c_int, [_i64, _i64, _i32, _i32, _i32, _i32, _i32, _i32, ctypes.c_uint64, _ptr,
+                                           _ptr, _ptr, _ptr]),
     "pam_p1_values_f64": (ctypes.c_int, [ctypes.c_int, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr]),
     "pam_csr_spmv_f64": (ctypes.c_int, [_i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr]),
     "pam_pcg_workspace_bytes": (_i64, [_i64]),

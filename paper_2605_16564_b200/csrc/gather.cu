@@ -207,15 +207,16 @@ __device__ void c5_box(uint64_t seed, int64_t s, int gx, int gy, C5Box& b) {
   for (int r = 0; r < (1 << b.k); ++r) b.lev[r] = exp10(-3.0 + 6.0 * u01(seed, s, 4, r));
 }
 
-__global__ void c5_points_kernel(int64_t n_sub, int n_pts, int gx, int gy, uint64_t seed, double* pts,
-                                 double* vals) {
+__global__ void c5_points_kernel(int64_t first, int64_t n_sub, int n_pts, int gx, int gy, uint64_t seed,
+                                 double* pts, double* vals) {
   __shared__ C5Box b;
-  for (int64_t s = blockIdx.x; s < n_sub; s += gridDim.x) {
+  for (int64_t ls = blockIdx.x; ls < n_sub; ls += gridDim.x) {
+    const int64_t s = first + ls;  // global box index (random stream), ls = output slot
     __syncthreads();
     if (threadIdx.x == 0) c5_box(seed, s, gx, gy, b);
     __syncthreads();
     for (int i = threadIdx.x; i < n_pts; i += blockDim.x) {
-      const int64_t row = s * n_pts + i;
+      const int64_t row = ls * n_pts + i;
       double x[3];
       for (int c = 0; c < 3; ++c) {
         x[c] = b.lo[c] + u01(seed, s, 5, 3 * static_cast<uint64_t>(i) + c);
@@ -232,14 +233,14 @@ __global__ void c5_points_kernel(int64_t n_sub, int n_pts, int gx, int gy, uint6
   }
 }
 
-__global__ void c5_centres_kernel(int64_t n_sub, int lx, int ly, int lz, int gx, int gy, uint64_t seed,
-                                  double* cen) {
+__global__ void c5_centres_kernel(int64_t first, int64_t n_sub, int lx, int ly, int lz, int gx, int gy,
+                                  uint64_t seed, double* cen) {
   const int M = lx * ly * lz;
   const double h[3] = {1.0 / lx, 1.0 / ly, 1.0 / lz};
   const int64_t total = n_sub * M;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t s = e / M;
+    const int64_t s = first + e / M;
     const int m = static_cast<int>(e % M);
     const int li[3] = {m % lx, (m / lx) % ly, m / (lx * ly)};
     const double lo[3] = {static_cast<double>(s % gx), static_cast<double>((s / gx) % gy),
@@ -254,15 +255,15 @@ __global__ void c5_centres_kernel(int64_t n_sub, int lx, int ly, int lz, int gx,
 
 }  // namespace pam
 
-extern "C" int pam_c5_generate_f64(int64_t n_sub, int32_t n_pts, int32_t lx, int32_t ly, int32_t lz,
-                                   int32_t gx, int32_t gy, uint64_t seed, double* points, double* values,
-                                   double* centres, void* stream) {
-  if (n_sub < 1 || n_pts < 1 || lx < 1 || ly < 1 || lz < 1 || gx < 1 || gy < 1) return PAM_ERR_ARG;
+extern "C" int pam_c5_generate_f64(int64_t first_box, int64_t n_sub, int32_t n_pts, int32_t lx, int32_t ly,
+                                   int32_t lz, int32_t gx, int32_t gy, uint64_t seed, double* points,
+                                   double* values, double* centres, void* stream) {
+  if (first_box < 0 || n_sub < 1 || n_pts < 1 || lx < 1 || ly < 1 || lz < 1 || gx < 1 || gy < 1) return PAM_ERR_ARG;
   cudaStream_t st = as_stream(stream);
   const int blocks = static_cast<int>(std::min<int64_t>(n_sub, 148 * 16));
-  c5_points_kernel<<<blocks, 256, 0, st>>>(n_sub, n_pts, gx, gy, seed, points, values);
+  c5_points_kernel<<<blocks, 256, 0, st>>>(first_box, n_sub, n_pts, gx, gy, seed, points, values);
   PAM_LAUNCH_CHECK("c5_points_kernel");
-  c5_centres_kernel<<<148 * 8, 256, 0, st>>>(n_sub, lx, ly, lz, gx, gy, seed, centres);
+  c5_centres_kernel<<<148 * 8, 256, 0, st>>>(first_box, n_sub, lx, ly, lz, gx, gy, seed, centres);
   PAM_LAUNCH_CHECK("c5_centres_kernel");
   return PAM_OK;
 }

@@ -236,7 +236,7 @@ def config5(M: int = 256, n_sub: int = 65536, n_pts: int = 1000, n_eval: int = 1
 
 
 def config5_device(M: int = 256, n_sub: int = 65536, n_pts: int = 1000, seed: int = 5,
-                   host_copy: bool = True) -> PackedSubdomains:
+                   host_copy: bool = True, first_box: int = 0) -> PackedSubdomains:
     """BASELINE config 5 inputs generated on the GPU (``pam_c5_generate_f64``).
 
     Same distributions as :func:`config5` (unit boxes of the 64x32x32 tiling,
@@ -245,22 +245,24 @@ def config5_device(M: int = 256, n_sub: int = 65536, n_pts: int = 1000, seed: in
     numpy generator's but are deterministic for a seed; the full 65,536-box
     sweep is generated in well under a second instead of minutes on the host.
     Host copies are made unless ``host_copy=False`` (then only ``device``).
+    ``first_box``: generate boxes first_box .. first_box + n_sub - 1 of the
+    tiling (a rank's shard; a box's data do not depend on the range).
     """
     from . import _native as nat
 
     torch = nat.torch_mod()
     gx, gy, gz = C5_GRID
-    if n_sub > gx * gy * gz:
-        raise ValueError("n_sub exceeds the 64x32x32 tiling")
+    if first_box + n_sub > gx * gy * gz:
+        raise ValueError("boxes beyond the 64x32x32 tiling")
     g = C5_LATTICE[M]
     dev = nat.device()
     d_pts = torch.empty(n_sub * n_pts * 3, dtype=torch.float64, device=dev)
     d_vals = torch.empty(n_sub * n_pts, dtype=torch.float64, device=dev)
     d_cen = torch.empty(n_sub * M * 3, dtype=torch.float64, device=dev)
-    nat.check(nat.lib().pam_c5_generate_f64(n_sub, n_pts, g[0], g[1], g[2], gx, gy, seed, nat.ptr(d_pts),
+    nat.check(nat.lib().pam_c5_generate_f64(first_box, n_sub, n_pts, g[0], g[1], g[2], gx, gy, seed, nat.ptr(d_pts),
                                             nat.ptr(d_vals), nat.ptr(d_cen), nat.stream_ptr()),
               "pam_c5_generate_f64")
-    idx = np.arange(n_sub)
+    idx = first_box + np.arange(n_sub)
     lo = np.stack([idx % gx, (idx // gx) % gy, idx // (gx * gy)], axis=1).astype(float)
     h = np.array([1.0 / g[0], 1.0 / g[1], 1.0 / g[2]])
     cfg = AdaptiveConfig(m_max=0, elastic=PRESET_ELASTIC, max_rounds=1)

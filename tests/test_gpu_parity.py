@@ -472,6 +472,12 @@ def test_c5_device_generator(cuda):
     np.testing.assert_array_equal(p.points, q.points)
     np.testing.assert_array_equal(p.values, q.values)
     np.testing.assert_array_equal(p.centres, q.centres)
+    # a rank's shard (boxes 16..39) holds exactly those boxes' data
+    sh = workloads.config5_device(M=64, n_sub=24, n_pts=1000, seed=11, first_box=16)
+    np.testing.assert_array_equal(sh.points, p.points[16000:40000])
+    np.testing.assert_array_equal(sh.values, p.values[16000:40000])
+    np.testing.assert_array_equal(sh.centres, p.centres[16 * 64:40 * 64])
+    np.testing.assert_array_equal(sh.box_lo, p.box_lo[16:40])
     pts = p.points.reshape(64, 1000, 3)
     assert np.all(pts >= p.box_lo[:, None, :]) and np.all(pts < p.box_hi[:, None, :])
     assert np.all(p.values >= 1e-3) and np.all(p.values <= 1e3)

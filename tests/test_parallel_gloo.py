@@ -24,6 +24,31 @@ def test_balanced_ranges():
     assert parallel.balanced_ranges(np.ones(3), 5)[-1][1] == 3
 
 
+def test_pack_unpack_round_trip():
+    """The allgatherv payload carries dictionaries, beta, generations and reports exactly."""
+    import paper_2605_16564_b200 as pam
+
+    rng = np.random.default_rng(3)
+    items = []
+    for k in range(4):
+        m = 3 + k
+        d = pam.RbfDictionary(centers=rng.random((m, 2)), widths=rng.uniform(0.1, 1, m),
+                              generations=rng.integers(0, 4, m))
+        reps = tuple(pam.RoundReport(r, m, r, *rng.random(4), 0.25) for r in range(k + 1))
+        beta = rng.standard_normal(m) * 10.0 ** rng.integers(-300, 300, m)
+        items.append((pam.LocalSurrogate(dictionary=d, beta=beta, log_transform=bool(k % 2)), reps))
+    back = parallel.unpack_results(parallel.pack_results(items, 2), 2)
+    for (l0, r0), (l1, r1) in zip(items, back):
+        np.testing.assert_array_equal(l0.dictionary.centers, l1.dictionary.centers)
+        np.testing.assert_array_equal(l0.dictionary.widths, l1.dictionary.widths)
+        np.testing.assert_array_equal(l0.dictionary.generations, l1.dictionary.generations)
+        np.testing.assert_array_equal(l0.beta, l1.beta)
+        assert l0.log_transform == l1.log_transform
+        assert r0 == r1
+    out = parallel.gather_packed(items, 0, 4, 4, 2)  # single process: no collective
+    assert [len(l.dictionary) for l, _ in out] == [3, 4, 5, 6]
+
+
 def _oracle_fit_range(field, part, cfg, sigma):
     from oracle import pam_oracle as O
     import paper_2605_16564_b200 as pam
@@ -82,6 +107,52 @@ def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         return s.getsockname()[1]
+
+
+def _dict_worker(rank, world, port, outq):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # rank r owns subdomains with sizes m_r (ragged, different counts per rank)
+        m = [np.array([3, 1, 4]), np.array([2, 5])][rank]
+        cap = m + 1  # capacity slots beyond the size stay unused
+        off = np.concatenate([[0], np.cumsum(cap)[:-1]])
+        L = int(cap.sum())
+        cen = np.arange(L * 2, dtype=np.float64) + 1000 * rank
+        wid = np.arange(L, dtype=np.float64) + 100 * rank
+        bet = -np.arange(L, dtype=np.float64) - 100 * rank
+        out = parallel.gather_device_dictionaries(torch.from_numpy(off), torch.from_numpy(m.astype(np.int32)),
+                                                  torch.from_numpy(cen), torch.from_numpy(wid),
+                                                  torch.from_numpy(bet), 2)
+        outq.put((rank, [t.numpy().tolist() for t in out]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_device_dictionary_allgatherv_gloo_world2():
+    """The packed device allgatherv (parallel.gather_device_dictionaries): ragged
+    ranges, rebased slot offsets, identical on both ranks."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dict_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][1] == res[1][1]
+    off, m, cen, wid, bet = res[0][1]
+    assert m == [3, 1, 4, 2, 5]
+    assert off == [0, 4, 6, 11, 14]  # rank 1's offsets rebased by rank 0's 11 slots
+    assert wid[:11] == list(range(11)) and wid[11:] == [100.0 + k for k in range(9)]
+    assert cen[22:24] == [1000.0, 1001.0] and bet[11] == -100.0
 
 
 def test_sharded_fit_gloo_world2_matches_single_process():
