@@ -668,7 +668,7 @@ def main():
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per CD launch from an ncu --set full capture (profiles/)")
     ap.add_argument("--tile-tau", type=float, default=None, help="CD tile-drop threshold (0 = dense stream)")
-    ap.add_argument("--cd-kernel", default=None, choices=["auto", "lean", "dual", "pair"])
+    ap.add_argument("--cd-kernel", default=None, choices=["auto", "lean", "dual", "pair", "block"])
     args = ap.parse_args()
     from paper_2605_16564_b200 import engine as E
 

@@ -688,16 +688,6 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_tile_kernel(const CdArgs a) {
 // mbarrier takes one arrival per half (lanes 0 and 16 issue their half's bulk
 // copy, or a plain arrival for an empty column).  Pairs are consecutive
 // entries of the longest-first order, so paired fits have similar work.
-__device__ __forceinline__ double half_sum(double v) {
-#pragma unroll
-  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-__device__ __forceinline__ double half_max(double v) {
-#pragma unroll
-  for (int o = 8; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
 
 template <int R, int STAGES, int WPC>
 __global__ void __launch_bounds__(WPC * 32, 1) cd_dual_kernel(const CdArgs a) {

@@ -49,6 +49,18 @@ __device__ __forceinline__ int tile_code(unsigned long long mk) {
 }
 __device__ __forceinline__ int code_tiles(int code) { return (code >> 8) & 0xff; }
 
+// 16-lane (half-warp) reductions of the two-fits-per-warp kernels
+__device__ __forceinline__ double half_sum(double v) {
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double half_max(double v) {
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
 inline int sm_count() {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
