@@ -24,22 +24,33 @@
 
 namespace pam {
 
-constexpr int GT_TILE = 32;
 
 // ---- G = W^T W -------------------------------------------------------------
+// Register-blocked FP64 tiles: a CTA of 256 threads computes one 64 x 64 block
+// (jb <= kb: the upper block triangle, mirrored on store) of G_s = W_s^T W_s,
+// each thread a 4 x 4 micro-tile (rows ty + 16u, columns tx + 16v: the two
+// operand fetches of a k-step are 4 + 4 conflict-free shared loads feeding 16
+// DFMA, vs 5 loads per 4 DFMA in a 32 x 32 one-output-per-thread tile).  W is
+// column-major with its rows (sample points) contiguous, so a K-chunk of 16
+// rows x 64 columns is staged with coalesced loads.  Each G entry is one
+// fixed-order FP64 sum over the rows (deterministic; SURVEY F3 rules out lower
+// precision).  gram_kernel ncu (r02, C5 M=512): FP64 pipe 27 % for the 32 x 32
+// version.
+constexpr int GB = 64;  // output block
+constexpr int GK = 16;  // rows per K-chunk
 __global__ void __launch_bounds__(256)
 gram_kernel(const int64_t* __restrict__ row_off, const int32_t* __restrict__ m_cur,
             const int64_t* __restrict__ w_off, const int32_t* __restrict__ ld,
             const int64_t* __restrict__ g_off, const int32_t* __restrict__ ldg,
             const int32_t* __restrict__ active, const double* __restrict__ W,
             double* __restrict__ G) {
-  __shared__ double A[GT_TILE][GT_TILE + 1];
-  __shared__ double B[GT_TILE][GT_TILE + 1];
+  __shared__ double A[GK][GB + 2];
+  __shared__ double B[GK][GB + 2];
   const int64_t s = blockIdx.y;
   if (active != nullptr && active[s] == 0) return;
   const int M = m_cur[s];
-  const int T = (M + GT_TILE - 1) / GT_TILE;
-  // decode upper-triangular tile pair (jb <= kb) from blockIdx.x
+  const int T = (M + GB - 1) / GB;
+  // decode upper-triangular block pair (jb <= kb) from blockIdx.x
   int pair = blockIdx.x, jb = 0;
   while (jb < T && pair >= T - jb) {
     pair -= T - jb;
@@ -50,35 +61,51 @@ gram_kernel(const int64_t* __restrict__ row_off, const int32_t* __restrict__ m_c
   const int n = static_cast<int>(row_off[s + 1] - row_off[s]);
   const double* Ws = W + w_off[s];
   const int64_t lds = ld[s];
-  double* Gs = G + g_off[s];
-  const int64_t ldgs = ldg[s];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int i0 = 0; i0 < n; i0 += GT_TILE) {
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;  // 16 x 16 threads, 4 x 4 outputs each
+  double acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+  // staging: thread -> (row i = tid % 16, column c = tid / 16 + 16 q), q < 4
+  const int si = tid & 15, sc = tid >> 4;
+  for (int i0 = 0; i0 < n; i0 += GK) {
     __syncthreads();
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int c = ty + 8 * u;
-      const int i = i0 + tx;
-      const int cj = jb * GT_TILE + c, ck = kb * GT_TILE + c;
-      A[tx][c] = (i < n && cj < M) ? Ws[(int64_t)cj * lds + i] : 0.0;
-      B[tx][c] = (i < n && ck < M) ? Ws[(int64_t)ck * lds + i] : 0.0;
+    for (int q = 0; q < 4; ++q) {
+      const int c = sc + 16 * q;
+      const int i = i0 + si;
+      const int cj = jb * GB + c, ck = kb * GB + c;
+      A[si][c] = (i < n && cj < M) ? Ws[(int64_t)cj * lds + i] : 0.0;
+      B[si][c] = (i < n && ck < M) ? Ws[(int64_t)ck * lds + i] : 0.0;
     }
     __syncthreads();
-#pragma unroll 8
-    for (int i = 0; i < GT_TILE; ++i) {
-      const double a = A[i][tx];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] = fma(a, B[i][ty + 8 * u], acc[u]);
+    for (int i = 0; i < GK; ++i) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) av[u] = A[i][ty + 16 * u];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) bv[v] = B[i][tx + 16 * v];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
     }
   }
-  const int j = jb * GT_TILE + tx;
+  double* Gs = G + g_off[s];
+  const int64_t ldgs = ldg[s];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
-    const int k = kb * GT_TILE + ty + 8 * u;
-    if (j < M && k < M) {
-      Gs[(int64_t)k * ldgs + j] = acc[u];
-      if (jb != kb) Gs[(int64_t)j * ldgs + k] = acc[u];
+    const int j = jb * GB + ty + 16 * u;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int k = kb * GB + tx + 16 * v;
+      if (j < M && k < M) {
+        Gs[(int64_t)k * ldgs + j] = acc[u][v];
+        if (jb != kb) Gs[(int64_t)j * ldgs + k] = acc[u][v];
+      }
     }
   }
 }
@@ -400,7 +427,7 @@ extern "C" int pam_gram_f64(int64_t S, const int64_t* row_off, const int32_t* m_
   if (S < 0 || max_m < 0) return PAM_ERR_ARG;
   if (S == 0 || max_m == 0) return PAM_OK;
   cudaStream_t st = as_stream(stream);
-  const int T = (max_m + GT_TILE - 1) / GT_TILE;
+  const int T = (max_m + GB - 1) / GB;
   for (int64_t s0 = 0; s0 < S; s0 += 65535) {
     const int64_t cnt = std::min<int64_t>(65535, S - s0);
     const int32_t* act = active ? active + s0 : nullptr;
