@@ -685,11 +685,13 @@ def load(source) -> GlobalSurrogate:
             raise DataError("surrogate file truncated: unexpected end of input")
         block = lines[pos:pos + n_entries]
         pos += n_entries
-        toks = " ".join(block).split()
-        if len(toks) != n_entries * (dim + 3):
-            for m, ln in enumerate(block):
-                if len(ln.split()) != dim + 3:
-                    raise DataError(f"malformed dictionary entry at subdomain {i} row {m}")
+        # every entry row has exactly dim + 3 tokens (a short row and a long row
+        # must not cancel out in the block total)
+        per_row = [ln.split() for ln in block]
+        for m, t in enumerate(per_row):
+            if len(t) != dim + 3:
+                raise DataError(f"malformed dictionary entry at subdomain {i} row {m}")
+        toks = [v for t in per_row for v in t]
         try:
             arr = np.array(toks, dtype=float).reshape(n_entries, dim + 3)
             gens = np.array(toks[dim + 2::dim + 3], dtype=np.int64)

@@ -142,6 +142,15 @@ def test_load_errors():
         pam.loads("something else entirely\n")
     with pytest.raises(pam.DataError, match="version"):
         pam.loads(text.replace("fieldfit-surrogate 1", "fieldfit-surrogate 99", 1))
+    # one entry row short, the next one long by the same amount: the block total
+    # still matches, the per-row check must catch it (reference partition.py:312)
+    lines = text.splitlines()
+    sub = next(k for k, ln in enumerate(lines) if ln.startswith("subdomain 0 "))
+    a, b = lines[sub + 1].split(), lines[sub + 2].split()
+    lines[sub + 1] = " ".join(a[:-1])
+    lines[sub + 2] = " ".join(b + [a[-1]])
+    with pytest.raises(pam.DataError, match="malformed dictionary entry at subdomain 0 row 0"):
+        pam.loads("\n".join(lines) + "\n")
 
 
 def test_reports_csv():
