@@ -78,7 +78,7 @@ int64_t pam_cd_max_rows(void);
 #define PAM_CD_LEAN 1 /* one fit per warp                                       */
 #define PAM_CD_DUAL 2 /* two fits per warp (257-512 rows)                       */
 #define PAM_CD_PAIR 3 /* column pairs, few fits per SM (33-1024 rows)           */
-#define PAM_CD_BLOCK 4 /* exact blocked CD, one 8-warp CTA per fit (<= 1024 rows) */
+#define PAM_CD_BLOCK 4 /* exact blocked CD, a solver + 8 worker warps per fit (<= 1024 rows) */
 
 /* err[0] = 0 (no error), err[1] = INT64_MAX. Device pointer. */
 int pam_err_reset(int64_t* err, void* stream);
@@ -197,9 +197,10 @@ int pam_cd_ex_f64(int64_t S, const int64_t* order, const int64_t* row_off, doubl
  * pam_cd_tiles_f64 is pam_cd_f64 over that layout: one cp.async.bulk of
  * popcount(mask)*256 bytes per column; y is read through perm; max_m = the
  * largest m_cur of the batch (host-known; sizes the few-fit kernel's
- * staging).  kernel = PAM_CD_AUTO: 257-1024-row fits with <= 1 fit per SM
+ * staging).  kernel = PAM_CD_AUTO: 257-1024-row fits with <= 2 fits per SM
  * run the exact blocked CD (a CTA per fit: block dots, in-block updates
- * through the diagonal Gram block, one block AXPY), with <= 3 fits per SM the
+ * through the diagonal Gram block, one block AXPY, pipelined across blocks
+ * with the previous-block Gram block), with <= 3 fits per SM the
  * column-pair kernel, 257-512-row fits with
  * >= 8 fits per SM two fits per warp, everything else one fit per warp;
  * results are the same either way up to dot-product rounding.  `work` as for

@@ -1523,13 +1523,13 @@ int launch_pair(const CdArgs& a, int max_rows, int max_m, cudaStream_t stream) {
 }
 
 // Tile-packed design matrices (<= 1024 rows).  Auto selection:
-//  * 257-1024 rows and <= 1 fit per SM: the exact blocked CD (cd_block.cu);
+//  * 257-1024 rows and <= 2 fits per SM: the exact blocked CD (cd_block.cu);
 //  * 257-1024 rows and <= 3 fits per SM: the column-pair kernel;
 //  * 257-512 rows and >= 8 fits per SM (C4): two fits per warp;
 //  * otherwise one fit per warp.
 int cd_auto_kernel(int64_t S, int max_rows) {
   const int64_t sms = sm_count();
-  if (max_rows > 256 && S <= sms) return PAM_CD_BLOCK;
+  if (max_rows > 256 && S <= 2 * sms) return PAM_CD_BLOCK;
   if (max_rows > 256 && S <= 3 * sms) return PAM_CD_PAIR;
   if (max_rows > 256 && max_rows <= 512 && S >= 8 * sms) return PAM_CD_DUAL;
   return PAM_CD_LEAN;

@@ -26,7 +26,7 @@ def test_library_exists_and_loads():
     assert lib.pam_cd_max_rows() >= 2**31 - 1  # no row envelope (elastic_net.py has none)
     assert lib.pam_cd_workspace_bytes(10, 5000, 700, 500, 1) == 256
     assert lib.pam_cd_workspace_bytes(1, 20000, 100, 20000, 0) == 256 + 8 * 20000
-    assert lib.pam_cd_workspace_bytes(4, 4000, 1000, 1000, 4) == 256 + 288 * 1000 + 32 * 4  # blocked CD
+    assert lib.pam_cd_workspace_bytes(4, 4000, 1000, 1000, 4) == 256 + 576 * 1000 + 96 * 4  # blocked CD
 
 
 def test_every_declared_symbol_is_exported_and_bound():
