@@ -106,9 +106,11 @@ def test_cd_oracle_random_instances(cuda):
         assert abs(res.objective - o["objective"]) <= 1e-10 * max(1, abs(o["objective"]))
 
 
-@pytest.mark.parametrize("n", [33, 700, 1500, 3000])
+@pytest.mark.parametrize("n", [33, 700, 1500, 3000, 8192, 8193, 20000])
 def test_cd_group_kernels_large_n(cuda, n):
-    # rows beyond one warp's register budget use the multi-warp group kernels
+    # rows beyond one warp's register budget use the multi-warp group kernels; above
+    # 8192 rows the CTA-per-fit kernel with the residual in the workspace (the
+    # reference has no row limit)
     rng = np.random.default_rng(n)
     m = 40
     W = np.abs(rng.standard_normal((n, m)))
@@ -241,3 +243,48 @@ def test_local_eval_far_points_use_exact_fallback(cuda):
     ref = O.surrogate_eval(pts, c, w, beta)
     assert np.isfinite(ref).all()
     np.testing.assert_allclose(loc.evaluate(pts), ref, rtol=1e-12)
+
+
+def test_cd_host_seam_large_n(cuda):
+    """pam_cd_sweeps_host_f64 (the _cd_sweeps_jit seam) above the register envelope."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    from integration import fieldfit_b200 as b
+
+    rng = np.random.default_rng(9)
+    n, m = 12000, 30
+    W = np.asfortranarray(np.abs(rng.standard_normal((n, m))))
+    y = rng.standard_normal(n)
+    col_sq = np.einsum("nm,nm->m", W, W)
+    beta, r, hist = np.zeros(m), y.copy(), np.empty(500)
+    sweeps, conv = b.cd_sweeps_b200(W, col_sq, col_sq + 1e-4, 1e-3, 1e-4, 1e-9, 500, beta, r, hist)
+    o = O.fit(np.ascontiguousarray(W), y, 1e-3, 1e-4, 1e-9, 500)
+    assert abs(sweeps - o["iterations"]) <= 1
+    assert np.max(np.abs(beta - o["beta"])) <= 1e-8 * max(1, np.abs(o["beta"]).max())
+    np.testing.assert_allclose(r, y - W @ beta, rtol=0, atol=1e-9 * np.abs(y).max())
+
+
+def test_unregularised_adaptive_fit_streams_every_entry(cuda):
+    """lam1 = lam2 = 0 (the ElasticNetConfig defaults): tile dropping is off (a column
+    whose entries are all below tau would otherwise lose its exact tiny col_sq, ADVICE
+    r01); the adaptive fit matches the bit-exact oracle."""
+    from paper_2605_16564_b200 import engine as E
+
+    field = pam.box_field_2d(16, 16)
+    sub = field.whole()
+    en = pam.ElasticNetConfig(lam1=0.0, lam2=0.0, tol=1e-8, max_iters=3000)
+    cfg = pam.AdaptiveConfig(k_top=12, m_max=72, eta=0.5, m_q=3, max_rounds=3, elastic=en,
+                             offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
+    sigma = 1.0 / 64  # narrow: far columns have every entry < 1e-16 in some rows
+    assert E.tile_tau() == 1e-16
+    with E.options(cd_form="residual"):
+        sur, reps = pam.fit_adaptive(sub, pam.centroid_dictionary(sub.centroids, sigma), cfg)
+    c = dict(lam1=0.0, lam2=0.0, tol=1e-8, max_iters=3000, k_top=12, m_max=72, eta=0.5, m_q=3, max_rounds=3,
+             offsets=cfg.offsets)
+    od = O.fit_adaptive(sub.centroids, sub.values, field.mesh.cell_size, sub.box.lo, sub.box.hi, sub.centroids,
+                        np.full(len(sub.values), sigma), c)
+    np.testing.assert_array_equal(sur.dictionary.centers, od["centers"])
+    assert np.max(np.abs(sur.beta - od["beta"])) <= 1e-8 * max(1, np.abs(od["beta"]).max())
+    assert [r.centers for r in reps] == [r["centers"] for r in od["reports"]]
