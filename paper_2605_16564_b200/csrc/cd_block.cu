@@ -59,14 +59,12 @@ __device__ __forceinline__ int col_pack(int rel, int code) { return rel | ((code
 template <int SLOT_WD, int GMAX, int MINB>
 __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsigned char* const ws) {
   constexpr int GD = GMAX * GMAX;
-  static_assert(GMAX <= 16, "the workers' partial dots are laid out 16 columns per warp");
-  static_assert(SLOT_WD <= NWK * 32 * 30, "a worker's dot range must stay below one 32-double column");
   constexpr int SLOT_D = SLOT_WD + 2 * GD;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* const slots = reinterpret_cast<double*>(smem_raw);
   double* const rs = slots + STAGES * SLOT_D;  // [1024] residual mirror (position order)
-  double* const zraw = rs + 1024;               // [2][NWK][16] per-warp partial block dots (element parity)
-  double* const dd = zraw + 2 * NWK * 16;       // [2][32] block steps, compacted to the nonzero ones
+  double* const zraw = rs + 1024;               // [2][32] block dots (element parity)
+  double* const dd = zraw + 64;                 // [2][32] block steps, compacted to the nonzero ones
   double* const dfull = dd + 64;                // [2][32] block steps by column (solver)
   double* const red = dfull + 64;               // [32] reductions (sweep-parity double-buffered)
   int* const par = reinterpret_cast<int*>(red + 32);  // [4][32] packed column parameters (element & 3)
@@ -285,51 +283,6 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
         r2[0] = make_double2(r[0], r[1]);
         r2[1] = make_double2(r[2], r[3]);
       };
-      // workers: all dots of a block at once.  The block's packed W is one
-      // contiguous run (columns back to back); worker thread wt takes the K (<= 22)
-      // consecutive doubles [wt K, wt K + K) -- at most one column boundary, since
-      // a column is >= 32 doubles -- and each warp reduces, per column it touched,
-      // its lanes' partial sums; out[warp][c] (fixed order over warps in the solver)
-      auto block_dots = [&](const double* Wb, const int* pk, int nb, double* out) {
-        const int cl = pk[nb - 1];
-        const int wlen = (cl & 0xffff) + 32 * (cl >> 24);
-        const int K = (((wlen + NWK * 32 - 1) / (NWK * 32)) + 1) & ~1;
-        const int i0 = min(wt * K, wlen), i1 = min(i0 + K, wlen);
-        int c = 0;
-        while (c + 1 < nb && (pk[c + 1] & 0xffff) <= i0) ++c;
-        const int c0 = c;
-        int cp = pk[c];
-        int o = cp & 0xffff, a0 = (cp >> 16) & 0xff;
-        int onext = (c + 1 < nb) ? (pk[c + 1] & 0xffff) : 0x7fffffff;
-        double s0a = 0.0, s0b = 0.0, s1a = 0.0, s1b = 0.0;
-        for (int i = i0; i < i1; i += 2) {
-          if (i >= onext) {
-            ++c;
-            cp = pk[c];
-            o = cp & 0xffff;
-            a0 = (cp >> 16) & 0xff;
-            onext = (c + 1 < nb) ? (pk[c + 1] & 0xffff) : 0x7fffffff;
-          }
-          const double2 w = *reinterpret_cast<const double2*>(Wb + i);
-          const double2 x = *reinterpret_cast<const double2*>(rs + 32 * a0 + (i - o));
-          if (c == c0) {
-            s0a = fma(w.x, x.x, s0a);
-            s0b = fma(w.y, x.y, s0b);
-          } else {
-            s1a = fma(w.x, x.x, s1a);
-            s1b = fma(w.y, x.y, s1b);
-          }
-        }
-        const double s0 = s0a + s0b, s1 = s1a + s1b;
-        const int c1 = c;
-        const int cA = __shfl_sync(0xffffffffu, c0, 0), cB = __shfl_sync(0xffffffffu, c1, 31);
-        double mine = 0.0;
-        for (int cc = cA; cc <= cB; ++cc) {
-          const double v = warp_sum((c0 == cc ? s0 : 0.0) + ((c1 == cc && c1 != c0) ? s1 : 0.0));
-          if (lane == cc) mine = v;
-        }
-        if (lane < 16) out[(warp - 1) * 16 + lane] = (lane >= cA && lane <= cB) ? mine : 0.0;
-      };
       // a warp's dot of packed column cp with rs (self: with itself) -> every lane
       auto col_dot = [&](const double* Wb, int cp, bool self) -> double {
         const int o = cp & 0xffff, a0 = (cp >> 16) & 0xff, la = cp >> 24;
@@ -448,7 +401,11 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
       cta_bar();
       if (!solver && total > 0) {  // pre-step: dots of element 0 against the prologue residual
         wait_next();
-        block_dots(slot_of(0), par, enb[0], zraw);
+        const double* Wb = slot_of(0);
+        for (int j = warp - 1; j < enb[0]; j += NWK) {
+          const double z = col_dot(Wb, par[j], false);
+          if (lane == 0) zraw[j] = z;
+        }
       }
       cta_bar();
 
@@ -488,13 +445,8 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
             const double* Wb = slot_of(t);
             const double* Gd = Wb + SLOT_WD;
             const double* Go = Wb + SLOT_WD + GD;
-            // z = (sum of the workers' partial dots) - G[t, t-1] d_{t-1}
-            double zdot = 0.0;
-            if (lane < nb) {
-              const double* zp = zraw + NWK * 16 * (t & 1) + lane;
-#pragma unroll
-              for (int w = 0; w < NWK; ++w) zdot += zp[16 * w];
-            }
+            // z = zraw - G[t, t-1] d_{t-1}
+            double zdot = (lane < nb) ? zraw[32 * (t & 1) + lane] : 0.0;
             if (t > 0 && lane < nb) {
               const double* dp = dfull + 32 * ((t - 1) & 1);
               const int nbp = bk.nbp;
@@ -587,7 +539,12 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
           if (!stopped && t + 1 < total) {
             const uint32_t e = t + 1;
             wait_next();
-            block_dots(slot_of(e), par + 32 * (e & 3), enb[e & 3], zraw + NWK * 16 * (e & 1));
+            const double* Wb = slot_of(e);
+            const int* pk = par + 32 * (e & 3);
+            for (int j = warp - 1; j < enb[e & 3]; j += NWK) {
+              const double z = col_dot(Wb, pk[j], false);
+              if (lane == 0) zraw[32 * (e & 1) + j] = z;
+            }
           }
           if (t > 0 && (t - 1) % nblk == static_cast<uint32_t>(nblk - 1)) {
             // the AXPY above completed sweep sw: its residual sum of squares
@@ -668,7 +625,7 @@ int64_t cd_block_workspace_bytes(int64_t S, int64_t total_slots) {
 template <int SLOT_WD, int GMAX, int MINB>
 int launch_block_pipe_cfg(const CdArgs& a, void* block_ws, cudaStream_t stream) {
   using namespace bp;
-  const size_t smem = static_cast<size_t>(STAGES) * (SLOT_WD + 2 * GMAX * GMAX) * 8 + (1024 + 2 * NWK * 16 + 64 * 2 + 32) * 8 +
+  const size_t smem = static_cast<size_t>(STAGES) * (SLOT_WD + 2 * GMAX * GMAX) * 8 + (1024 + 64 * 3 + 32) * 8 +
                       (128 + 4 + 64 + 2 + 10) * 4 + 8 * STAGES + 16;
   auto kernel = cd_block_kernel<SLOT_WD, GMAX, MINB>;
   PAM_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

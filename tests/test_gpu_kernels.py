@@ -266,25 +266,33 @@ def test_cd_host_seam_large_n(cuda):
     np.testing.assert_allclose(r, y - W @ beta, rtol=0, atol=1e-9 * np.abs(y).max())
 
 
-def test_unregularised_adaptive_fit_streams_every_entry(cuda):
-    """lam1 = lam2 = 0 (the ElasticNetConfig defaults): tile dropping is off (a column
-    whose entries are all below tau would otherwise lose its exact tiny col_sq, ADVICE
-    r01); the adaptive fit matches the bit-exact oracle."""
+def test_unregularised_fits_stream_every_entry(cuda):
+    """lam1 = 0 (the ElasticNetConfig default): tile dropping is off -- a column whose
+    entries are all below tau would lose its exact tiny col_sq, and with lam2 = 0 the
+    reference divides by it (ADVICE r01) -- and the fit matches the bit-exact oracle;
+    with lam1 > 0 the same batch streams tiles."""
     from paper_2605_16564_b200 import engine as E
 
     field = pam.box_field_2d(16, 16)
     sub = field.whole()
-    en = pam.ElasticNetConfig(lam1=0.0, lam2=0.0, tol=1e-8, max_iters=3000)
-    cfg = pam.AdaptiveConfig(k_top=12, m_max=72, eta=0.5, m_q=3, max_rounds=3, elastic=en,
-                             offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
-    sigma = 1.0 / 64  # narrow: far columns have every entry < 1e-16 in some rows
-    assert E.tile_tau() == 1e-16
-    with E.options(cd_form="residual"):
-        sur, reps = pam.fit_adaptive(sub, pam.centroid_dictionary(sub.centroids, sigma), cfg)
-    c = dict(lam1=0.0, lam2=0.0, tol=1e-8, max_iters=3000, k_top=12, m_max=72, eta=0.5, m_q=3, max_rounds=3,
-             offsets=cfg.offsets)
-    od = O.fit_adaptive(sub.centroids, sub.values, field.mesh.cell_size, sub.box.lo, sub.box.hi, sub.centroids,
-                        np.full(len(sub.values), sigma), c)
-    np.testing.assert_array_equal(sur.dictionary.centers, od["centers"])
-    assert np.max(np.abs(sur.beta - od["beta"])) <= 1e-8 * max(1, np.abs(od["beta"]).max())
-    assert [r.centers for r in reps] == [r["centers"] for r in od["reports"]]
+    sigma = 1.0 / 16
+    cen = sub.centroids
+    for lam1, tiles in ((0.0, False), (4.59e-4, True)):
+        en = pam.ElasticNetConfig(lam1=lam1, lam2=0.0, tol=1e-10, max_iters=20000)
+        cfg = pam.AdaptiveConfig(m_max=0, elastic=en)
+        with E.options(cd_form="residual"):
+            eng = E.FitEngine(2, field.mesh.cell_size, np.array([0, len(sub.values)]),
+                              nat_dev(cen.reshape(-1)), nat_dev(sub.values), np.array([sub.box.lo]),
+                              np.array([sub.box.hi]), [cfg], centroid_sigma=np.array([sigma]))
+            assert eng.tiles is tiles and (eng.tau > 0) is tiles
+            res = eng.run()
+        W = O.shepard_features(cen, cen, np.full(len(cen), sigma))
+        o = O.fit_log(sub.values, W, lam1, 0.0, 1e-10, 20000)
+        assert np.max(np.abs(res.beta[0] - o["beta"])) <= 1e-8 * max(1, np.abs(o["beta"]).max())
+        assert abs(int(res.rounds[0].sweeps[0]) - o["iterations"]) <= 1
+
+
+def nat_dev(a):
+    from paper_2605_16564_b200 import _native as nat
+
+    return nat.to_dev(np.ascontiguousarray(a, dtype=np.float64))
