@@ -37,14 +37,32 @@
 #include "cd_common.cuh"
 
 #include <algorithm>
+#include <cstdio>
 
 namespace pam {
 
 namespace bp {
 
+#ifdef PAM_BLK_PROF
+#define PROF_DECL long long pf_t[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long pf_c = 0;
+#define PROF_START pf_c = clock64();
+#define PROF_LAP(i) { const long long pf_n = clock64(); pf_t[i] += pf_n - pf_c; pf_c = pf_n; }
+#else
+#define PROF_DECL
+#define PROF_START
+#define PROF_LAP(i)
+#endif
+
 constexpr int STAGES = 4;       // blocks t-1 (AXPY), t (solve), t+1 (dots), t+2 (in flight)
-constexpr int NWK = 8;          // worker warps
-constexpr int NT = (NWK + 1) * 32;  // + solver warp 0
+#ifndef PAM_BLK_NWK
+#define PAM_BLK_NWK 8
+#endif
+constexpr int NWK = PAM_BLK_NWK;    // worker warps
+constexpr int NT = (NWK + 2) * 32;  // + solver warp 0 + stream warp NWK + 1
+constexpr int DT = (NWK + 1) * 32;  // the stream warp's issuing thread
+constexpr int RPT = 1024 / (NWK * 32);  // residual rows per worker thread (= tiles per worker warp)
+static_assert(RPT == 2 || RPT == 4, "worker row ownership: two or four consecutive rows per thread");
+constexpr int LCAP = 16;            // entries per worker warp's AXPY list (= GMAX)
 constexpr int64_t WS_PER_SLOT = 576;  // 32 B descriptor + 2 x 33 Gram doubles (+ padding) per slot
 constexpr int64_t WS_PER_FIT = 96;
 
@@ -63,19 +81,22 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* const slots = reinterpret_cast<double*>(smem_raw);
   double* const rs = slots + STAGES * SLOT_D;  // [1024] residual mirror (position order)
-  double* const zraw = rs + 1024;               // [2][32] block dots (element parity)
-  double* const dd = zraw + 64;                 // [2][32] block steps, compacted to the nonzero ones
-  double* const dfull = dd + 64;                // [2][32] block steps by column (solver)
-  double* const red = dfull + 64;               // [32] reductions (sweep-parity double-buffered)
-  int* const par = reinterpret_cast<int*>(red + 32);  // [4][32] packed column parameters (element & 3)
+  double* const zraw = rs + 1024;               // [2][2][16] block dots (element parity, run half, column)
+  double* const ldv = zraw + 64;                // [2][NWK][LCAP] nonzero block steps, per worker warp
+  double* const dfull = ldv + 2 * NWK * LCAP;   // [2][32] block steps by column (solver)
+  double* const red = dfull + 64;               // [64] reductions (sweep-parity double-buffered)
+  double* const sprm = red + 64;                // [16][4] solver: {beta, 1/denom, denom, G[k][k-1]} of column k
+  int* const par = reinterpret_cast<int*>(sprm + 64);  // [4][32] packed column parameters (element & 3)
   int* const enb = par + 128;                         // [4] columns of element (e & 3)
-  int* const nzi = enb + 4;                           // [2][32] columns of the nonzero steps
-  int* const enz = nzi + 64;                          // [2] nonzero steps of the element
-  int* const ctl = enz + 2;  // [8]: nblk, next item, stop flags [2] (step parity), sweeps done, converged
+  int* const lcp = enb + 4;                           // [2][NWK][LCAP] packed parameters of the listed columns
+  int* const lcnt = lcp + 2 * NWK * LCAP;             // [2][NWK] entries of each worker warp's list
+  int* const ctl = lcnt + 2 * NWK;  // [10]: nblk, next item, stop flags [2] (step parity), sweeps done, converged
   uint64_t* const bars = reinterpret_cast<uint64_t*>(ctl + 10);  // 8-byte aligned
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool solver = warp == 0;
-  const int wt = tid - 32;  // worker thread index (0..255), rows 4 wt .. 4 wt + 3
+  const bool worker = warp >= 1 && warp <= NWK;
+  const bool streamer = warp == NWK + 1;  // descriptor / parameter pipeline and the bulk copies
+  const int wt = tid - 32;  // worker thread index, rows RPT wt .. RPT wt + RPT - 1
   const uint32_t slots_s = smem_u32(slots);
   const uint32_t bars_s = smem_u32(bars);
 
@@ -150,12 +171,14 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
           ctl[0] = nb;
         }
       }
-      // residual rows 4 wt .. 4 wt + 3 (workers; position order, perm -> local row)
-      double r[4] = {0.0, 0.0, 0.0, 0.0};
-      if (!solver) {
+      // residual rows RPT wt .. (workers; position order, perm -> local row)
+      double r[RPT];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int p = 4 * wt + k;
+      for (int k = 0; k < RPT; ++k) r[k] = 0.0;
+      if (worker) {
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+          const int p = RPT * wt + k;
           const int row = a.perm ? (p < N ? a.perm[r0 + p] : 0) : p;
           r[k] = (p < N) ? a.y[r0 + row] : 0.0;
           rs[p] = r[k];
@@ -169,10 +192,10 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
       //      once, in order (`seen`), so no wait ever lags a slot by two phases
       Blk ibk;  // thread 32: descriptor of its next issue (loaded one issue ahead)
       auto iload = [&](int b) {
-        if (tid == 32) ibk = blk[b];
+        if (tid == DT) ibk = blk[b];
       };
       auto issue = [&](uint32_t e, bool with_g, int b_next) {
-        if (tid == 32) {
+        if (tid == DT) {
           const Blk bk = ibk;
           const int st = (ebase + e) % STAGES;
           const uint32_t wbytes = static_cast<uint32_t>(bk.wlen) * 8u;
@@ -222,92 +245,137 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
         par[32 * k + lane] = pf_par;
         if (lane == 0) enb[k] = pf_nb;
       };
-      // workers: rows -= sum_j d_j W_j over the block in slot Wb (d == 0 skipped)
-      auto axpy = [&](const double* Wb, const double* dsrc, const int* pk, int nb) {
-        const int tile = (4 * wt) >> 5;
-        const int sub = (4 * wt) & 31;
-        for (int j = 0; j < nb; ++j) {
-          const double dj = dsrc[j];
-          if (dj == 0.0) continue;
-          const int cp = pk[j];
-          const int o = cp & 0xffff, a0 = (cp >> 16) & 0xff, la = cp >> 24;
-          if (static_cast<unsigned>(tile - a0) < static_cast<unsigned>(la)) {
-            const double2* w2 = reinterpret_cast<const double2*>(Wb + o + 32 * (tile - a0) + sub);
-            const double2 u = w2[0], v = w2[1];
-            r[0] = fma(-dj, u.x, r[0]);
-            r[1] = fma(-dj, u.y, r[1]);
-            r[2] = fma(-dj, v.x, r[2]);
-            r[3] = fma(-dj, v.y, r[3]);
+      // workers: rows -= sum_k dv[k] W_{column cpv[k]} over cnt columns of the block in
+      // slot Wb, four columns per pass (all four columns' loads are in flight before
+      // the FMAs; a column outside this thread's tile, or past cnt, contributes an
+      // exact zero step), in ascending k
+      auto axpy_cols = [&](const double* Wb, const double* dv, const int* cpv, int cnt) {
+        const int tile = (RPT * wt) >> 5;
+        const int sub = (RPT * wt) & 31;
+        for (int k = 0; k < cnt; k += 4) {
+          double d[4];
+          double2 w[4][RPT / 2];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const bool ok = k + u < cnt;
+            const int kk = ok ? k + u : k;
+            const int cp = cpv[kk];
+            const int o = cp & 0xffff, a0 = (cp >> 16) & 0xff, la = cp >> 24;
+            const bool in = ok && static_cast<unsigned>(tile - a0) < static_cast<unsigned>(la);
+            const double2* w2 = reinterpret_cast<const double2*>(Wb + (in ? o + 32 * (tile - a0) + sub : 0));
+#pragma unroll
+            for (int v = 0; v < RPT / 2; ++v) w[u][v] = w2[v];
+            d[u] = in ? dv[kk] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+#pragma unroll
+            for (int v = 0; v < RPT / 2; ++v) {
+              r[2 * v] = fma(-d[u], w[u][v].x, r[2 * v]);
+              r[2 * v + 1] = fma(-d[u], w[u][v].y, r[2 * v + 1]);
+            }
           }
         }
-        double2* r2 = reinterpret_cast<double2*>(rs + 4 * wt);
-        r2[0] = make_double2(r[0], r[1]);
-        r2[1] = make_double2(r[2], r[3]);
+        double2* r2 = reinterpret_cast<double2*>(rs + RPT * wt);
+#pragma unroll
+        for (int v = 0; v < RPT / 2; ++v) r2[v] = make_double2(r[2 * v], r[2 * v + 1]);
       };
-      // workers, sweeps: rows -= d_k W_{col k} over the compacted nonzero steps
-      auto axpy_nz = [&](const double* Wb, const double* dnz, const int* idx, int cnt, const int* pk) {
-        const int tile = (4 * wt) >> 5;
-        const int sub = (4 * wt) & 31;
-        // two columns per pass: both columns' loads are in flight before the FMAs
-        // (a column outside this thread's tile contributes an exact zero step)
-        auto term = [&](int k, double& dj, double2& u, double2& v) {
-          const int cp = pk[idx[k]];
-          const int o = cp & 0xffff, a0 = (cp >> 16) & 0xff, la = cp >> 24;
-          const bool in = static_cast<unsigned>(tile - a0) < static_cast<unsigned>(la);
-          const double2* w2 = reinterpret_cast<const double2*>(Wb + (in ? o + 32 * (tile - a0) + sub : 0));
-          u = w2[0];
-          v = w2[1];
-          dj = in ? dnz[k] : 0.0;
-        };
-        int k = 0;
-        for (; k + 1 < cnt; k += 2) {
-          double da, db;
-          double2 ua, va, ub, vb;
-          term(k, da, ua, va);
-          term(k + 1, db, ub, vb);
-          r[0] = fma(-db, ub.x, fma(-da, ua.x, r[0]));
-          r[1] = fma(-db, ub.y, fma(-da, ua.y, r[1]));
-          r[2] = fma(-db, vb.x, fma(-da, va.x, r[2]));
-          r[3] = fma(-db, vb.y, fma(-da, va.y, r[3]));
-        }
-        if (k < cnt) {
-          double da;
-          double2 ua, va;
-          term(k, da, ua, va);
-          r[0] = fma(-da, ua.x, r[0]);
-          r[1] = fma(-da, ua.y, r[1]);
-          r[2] = fma(-da, va.x, r[2]);
-          r[3] = fma(-da, va.y, r[3]);
-        }
-        double2* r2 = reinterpret_cast<double2*>(rs + 4 * wt);
-        r2[0] = make_double2(r[0], r[1]);
-        r2[1] = make_double2(r[2], r[3]);
-      };
-      // a warp's dot of packed column cp with rs (self: with itself) -> every lane
-      auto col_dot = [&](const double* Wb, int cp, bool self) -> double {
+      // a warp's dot of packed column cp with rs (self: with itself) -> every lane.
+      // The run's double2 elements are taken in chunks of 32 (one per lane); with
+      // nh == 2 this warp takes the chunks of parity h (the other half goes to a
+      // second warp and the two partial sums are added by the consumer).
+      auto col_dot = [&](const double* Wb, int cp, bool self, int h, int nh) -> double {
         const int o = cp & 0xffff, a0 = (cp >> 16) & 0xff, la = cp >> 24;
         const double2* w2 = reinterpret_cast<const double2*>(Wb + o);
         const double2* x2 = reinterpret_cast<const double2*>(rs + 32 * a0);
         const int n2 = 16 * la;  // double2 elements of the run
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        int i = lane;
-        for (; i + 32 < n2; i += 64) {  // two independent element pairs per lane per pass
-          const double2 wa = w2[i], wb = w2[i + 32];
-          const double2 xa = self ? wa : x2[i], xb = self ? wb : x2[i + 32];
+        const int step = 32 * nh;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0, s5 = 0.0, s6 = 0.0, s7 = 0.0;
+        int i = lane + 32 * h;
+        for (; i + 3 * step < n2; i += 4 * step) {  // four independent element pairs per lane per pass
+          const double2 wa = w2[i], wb = w2[i + step], wc = w2[i + 2 * step], wd = w2[i + 3 * step];
+          const double2 xa = self ? wa : x2[i], xb = self ? wb : x2[i + step];
+          const double2 xc = self ? wc : x2[i + 2 * step], xd = self ? wd : x2[i + 3 * step];
           s0 = fma(wa.x, xa.x, s0);
           s1 = fma(wa.y, xa.y, s1);
           s2 = fma(wb.x, xb.x, s2);
           s3 = fma(wb.y, xb.y, s3);
+          s4 = fma(wc.x, xc.x, s4);
+          s5 = fma(wc.y, xc.y, s5);
+          s6 = fma(wd.x, xd.x, s6);
+          s7 = fma(wd.y, xd.y, s7);
         }
-        if (i < n2) {
+        for (; i < n2; i += step) {
           const double2 wa = w2[i];
           const double2 xa = self ? wa : x2[i];
           s0 = fma(wa.x, xa.x, s0);
           s1 = fma(wa.y, xa.y, s1);
         }
-        return warp_sum((s0 + s1) + (s2 + s3));
+        return warp_sum(((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7)));
       };
-
+      // two columns at once (one warp): both columns' loads and reductions interleave
+      auto col_dot2 = [&](const double* Wb, int cpa, int cpb, double& za, double& zb2) {
+        const int oa = cpa & 0xffff, aa = (cpa >> 16) & 0xff, la_ = cpa >> 24;
+        const int ob = cpb & 0xffff, ab = (cpb >> 16) & 0xff, lb_ = cpb >> 24;
+        const double2* wa2 = reinterpret_cast<const double2*>(Wb + oa);
+        const double2* xa2 = reinterpret_cast<const double2*>(rs + 32 * aa);
+        const double2* wb2 = reinterpret_cast<const double2*>(Wb + ob);
+        const double2* xb2 = reinterpret_cast<const double2*>(rs + 32 * ab);
+        const int na = 16 * la_, nbb = 16 * lb_;
+        const int nmax = max(na, nbb);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+        const double2 zz = make_double2(0.0, 0.0);
+        for (int i = lane; i < nmax; i += 64) {
+          const bool pa0 = i < na, pa1 = i + 32 < na, pb0 = i < nbb, pb1 = i + 32 < nbb;
+          const double2 w0 = pa0 ? wa2[i] : zz, w1 = pa1 ? wa2[i + 32] : zz;
+          const double2 v0 = pb0 ? wb2[i] : zz, v1 = pb1 ? wb2[i + 32] : zz;
+          const double2 x0 = pa0 ? xa2[i] : zz, x1 = pa1 ? xa2[i + 32] : zz;
+          const double2 y0 = pb0 ? xb2[i] : zz, y1 = pb1 ? xb2[i + 32] : zz;
+          a0 = fma(w0.x, x0.x, a0);
+          a1 = fma(w0.y, x0.y, a1);
+          a2 = fma(w1.x, x1.x, a2);
+          a3 = fma(w1.y, x1.y, a3);
+          b0 = fma(v0.x, y0.x, b0);
+          b1 = fma(v0.y, y0.y, b1);
+          b2 = fma(v1.x, y1.x, b2);
+          b3 = fma(v1.y, y1.y, b3);
+        }
+        double sa = (a0 + a1) + (a2 + a3), sb = (b0 + b1) + (b2 + b3);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          sa += __shfl_xor_sync(0xffffffffu, sa, o);
+          sb += __shfl_xor_sync(0xffffffffu, sb, o);
+        }
+        za = sa;
+        zb2 = sb;
+      };
+      // workers: the dots of a block of nb columns against rs -> zraw buffer zb
+      // ([2][16]: run half, column).  nb <= NWK / 2: two warps per column (run
+      // halves); nb <= NWK: one warp per column; more: columns w and w + NWK on
+      // warp w, interleaved.  Unsplit columns get a zero second half.
+      auto block_dots = [&](const double* Wb, const int* pk, int nb, double* zb) {
+        const int w = warp - 1;
+        if (nb <= NWK / 2) {
+          const int j = w % (NWK / 2), h = w / (NWK / 2);
+          if (j < nb) {
+            const double z = col_dot(Wb, pk[j], false, h, 2);
+            if (lane == 0) zb[16 * h + j] = z;
+          }
+        } else if (w < nb) {
+          double z0, z1 = 0.0;
+          const bool two = w + NWK < nb;
+          if (two) col_dot2(Wb, pk[w], pk[w + NWK], z0, z1);
+          else z0 = col_dot(Wb, pk[w], false, 0, 1);
+          if (lane == 0) {
+            zb[w] = z0;
+            zb[16 + w] = 0.0;
+            if (two) {
+              zb[w + NWK] = z1;
+              zb[16 + w + NWK] = 0.0;
+            }
+          }
+        }
+      };
       // ---- prologue pass: col_sq (elastic_net.py:85), r = y - W beta0 (94), and the
       //      diagonal and previous-block Gram blocks; elements 0..nblk-1, then block 0
       //      once more for G[0, nblk-1] (block 0 follows block nblk-1 across sweeps)
@@ -332,8 +400,8 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
           const double* Wb = slot_of(e);
           const int* pk = par + 32 * (e & 3);
           if (!wrap) {
-            for (int j = warp; j < nb; j += NWK + 1) {
-              const double cs = col_dot(Wb, pk[j], true);
+            for (int j = warp; j < nb; j += NWK + 2) {
+              const double cs = col_dot(Wb, pk[j], true, 0, 1);
               if (lane == 0) colsq[bk.j0 + j] = cs;
             }
           }
@@ -363,7 +431,7 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
             }
             Gf[(diag ? bk.gd : bk.go) + k * nb + c] = g;
           }
-          if (!wrap && !solver) axpy(Wb, zraw, pk, nb);  // r -= W_b beta0_b
+          if (!wrap && worker) axpy_cols(Wb, zraw, pk, nb);  // r -= W_b beta0_b
           asm volatile("fence.proxy.async.global;" ::: "memory");  // the sweeps re-read G by TMA
           cta_bar();  // slot e-1 free, rs current
           if (q < np_el) {
@@ -376,36 +444,45 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
 
       // ---- sweeps: one continuous stream of blocks, element t = block t % nblk of
       //      sweep t / nblk.  Step t: solver -> block t; workers -> AXPY of t-1, dots of t+1.
+      //      Block and sweep indices are carried incrementally (bcur, swc, qb): a
+      //      division by the run-time nblk costs ~40 instructions on every warp.
       const uint32_t total = static_cast<uint32_t>(nblk) * static_cast<uint32_t>(max_iters);
+      auto modn = [&](int x) -> int {
+        while (x >= nblk) x -= nblk;
+        return x;
+      };
       seen = 0;
       uint32_t q = 0;
+      int qb = 0;  // q % nblk
       iload(0);
-      for (; q < min(static_cast<uint32_t>(STAGES - 1), total); ++q) issue(q, true, static_cast<int>((q + 1) % nblk));
-      if (total > 0 && warp == 1) {
-        pfetch(0);
-        publish(0);
+      for (; q < min(static_cast<uint32_t>(STAGES - 1), total); ++q) {
+        const int qn = modn(qb + 1);
+        issue(q, true, qn);
+        qb = qn;
       }
-      if (total > 1 && warp == 2) {
-        pfetch(1 % nblk);
-        publish(1);
+      if (streamer) {
+        if (total > 0) {
+          pfetch(0);
+          publish(0);
+        }
+        if (total > 1) {
+          pfetch(modn(1));
+          publish(1);
+        }
+        if (total > 2) {
+          pfetch(modn(2));          // published at step 0
+          pfetch_d(blk[modn(3)]);   // packed at step 0, published at step 1
+          pd = blk[modn(4)];        // columns loaded at step 0
+        }
       }
-      if (total > 2 && warp == NWK) {
-        pfetch(2 % nblk);  // published at step 0
-        pfetch_d(blk[3 % nblk]);  // packed at step 0, published at step 1
-        pd = blk[4 % nblk];       // columns loaded at step 0
-      }
-      if (tid < 2) enz[tid] = 0;
-      if (tid < 64) dd[tid] = dfull[tid] = 0.0;
+      if (tid < 2 * NWK) lcnt[tid] = 0;
+      if (tid < 64) dfull[tid] = 0.0;
       if (tid < 2) ctl[2 + tid] = 0;  // stop flags (step parity)
       if (tid == 0) ctl[4] = ctl[5] = 0;  // sweeps done, converged
       cta_bar();
-      if (!solver && total > 0) {  // pre-step: dots of element 0 against the prologue residual
+      if (worker && total > 0) {  // pre-step: dots of element 0 against the prologue residual
         wait_next();
-        const double* Wb = slot_of(0);
-        for (int j = warp - 1; j < enb[0]; j += NWK) {
-          const double z = col_dot(Wb, par[j], false);
-          if (lane == 0) zraw[j] = z;
-        }
+        block_dots(slot_of(0), par, enb[0], zraw);
       }
       cta_bar();
 
@@ -420,15 +497,19 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
       };
       if (solver && total > 0) {
         sd_n1 = blk[0];
-        sd_n2 = blk[1 % nblk];
+        sd_n2 = blk[modn(1)];
         sprefetch(sd_n1);
       }
       double max_delta = 0.0, acc_l1 = 0.0, acc_l2 = 0.0, acc_max = 0.0;  // solver, per sweep
+      double corr = 0.0;  // solver: G[t, t-1] d_{t-1} of this lane's column (accumulated during step t-1)
+      int bcur = 0, swc = 0;  // t % nblk, t / nblk
+      PROF_DECL
       for (uint32_t t = 0; total > 0; ++t) {
         const bool stopped = ctl[2 + ((t + 1) & 1)] != 0;  // set by the solver at step t-1
+        const bool sweep_closed = t > 0 && bcur == 0;      // step t-1 was the last block of sweep swc - 1
+        PROF_START
         if (solver) {
           if (!stopped) {
-            const int b = static_cast<int>(t % nblk);
             sd_cur = sd_n1;
             sd_n1 = sd_n2;
             const Blk& bk = sd_cur;
@@ -440,62 +521,105 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
             const double dnc = __dadd_rn(csc, lam2);
             const double invc = dnc > 0.0 ? __ddiv_rn(1.0, dnc) : 0.0;
             if (nblk > 1 && t + 1 < total) sprefetch(sd_n1);  // its betas were written by this lane
-            if (t + 2 < total) sd_n2 = blk[(t + 2) % nblk];
-            wait_next();
+            if (t + 2 < total) sd_n2 = blk[modn(bcur + 2)];
+            PROF_LAP(0)
+            if (seen <= t) wait_next();
+            PROF_LAP(1)
             const double* Wb = slot_of(t);
             const double* Gd = Wb + SLOT_WD;
-            const double* Go = Wb + SLOT_WD + GD;
-            // z = zraw - G[t, t-1] d_{t-1}
-            double zdot = (lane < nb) ? zraw[32 * (t & 1) + lane] : 0.0;
-            if (t > 0 && lane < nb) {
-              const double* dp = dfull + 32 * ((t - 1) & 1);
-              const int nbp = bk.nbp;
-              double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
-              int i = 0;
-              for (; i + 4 <= nbp; i += 4) {
-                c0 = fma(Go[i * nb + lane], dp[i], c0);
-                c1 = fma(Go[(i + 1) * nb + lane], dp[i + 1], c1);
-                c2 = fma(Go[(i + 2) * nb + lane], dp[i + 2], c2);
-                c3 = fma(Go[(i + 3) * nb + lane], dp[i + 3], c3);
+            // the next block's previous-block Gram block G[t+1, t] (its slot landed a
+            // step ago): the term -G[t+1, t] d_t of the next step's dots is accumulated
+            // inside this step's update loop, off the serial chain
+            const bool has_next = t + 1 < total;
+            if (has_next && seen <= t + 1) wait_next();
+            const double* Go1 = slot_of(t + 1) + SLOT_WD + GD;
+            const int nb1 = has_next ? sd_n1.nb : 0;
+            // z = (zraw - G[t, t-1] d_{t-1}) + col_sq beta; lane c <-> column c
+            const double* zb = zraw + 32 * (t & 1);
+            const double zdot = (lane < nb) ? __dsub_rn(zb[lane] + zb[16 + lane], corr) : 0.0;
+            double zc = __dadd_rn(__dmul_rn(csc, bc), zdot);
+            // per-column constants, broadcast-read inside the loop (columns >= nb:
+            // zeros, so a padded step is exactly d = 0)
+            {
+              const bool on = lane < nb;
+              const double gp = (on && lane > 0) ? Gd[(lane - 1) * nb + lane] : 0.0;  // G[lane][lane-1]
+              if (lane < 16) {
+                double2* sp = reinterpret_cast<double2*>(sprm + 4 * lane);
+                sp[0] = make_double2(on ? bc : 0.0, on ? invc : 0.0);
+                sp[1] = make_double2(on ? dnc : 0.0, gp);
               }
-              for (; i < nbp; ++i) c0 = fma(Go[i * nb + lane], dp[i], c0);
-              zdot = __dsub_rn(zdot, (c0 + c1) + (c2 + c3));
             }
-            // the block's cyclic updates (elastic_net.py:137-156)
+            __syncwarp();
+            PROF_LAP(2)
+            // the block's cyclic updates (elastic_net.py:137-156).  Lane c carries
+            // zc = col_sq_c beta_c + W_c . r with the block's earlier steps applied;
+            // column k's value is broadcast one step EARLY (before step k-1 is known)
+            // and step k-1's term -d_{k-1} G[k][k-1] is applied to the broadcast copy,
+            // so the shuffle is off the serial chain: per column the chain is one FMA,
+            // the soft threshold and the step difference.  Four columns per
+            // straight-line group (operand loads hoist above the chain).
+            const int pkc = par[32 * (t & 3) + lane];  // this lane's column parameters (for the AXPY lists)
             double dc = 0.0;
-            for (int k = 0; k < nb; ++k) {
-              const double zk = __shfl_sync(0xffffffffu, zdot, k);
-              const double b_old = __shfl_sync(0xffffffffu, bc, k);
-              const double cs = __shfl_sync(0xffffffffu, csc, k);
-              const double inv = __shfl_sync(0xffffffffu, invc, k);
-              const double dn = __dadd_rn(cs, lam2);
-              const double z = __dadd_rn(__dmul_rn(cs, b_old), zk);
-              const double np_ = __dsub_rn(z, lam1), nn_ = __dadd_rn(z, lam1);
-              const double qp = __dmul_rn(np_, inv), qn = __dmul_rn(nn_, inv);
-              const double bp = fma(fma(-qp, dn, np_), inv, qp);
-              const double bn = fma(fma(-qn, dn, nn_), inv, qn);
-              const double b_new = np_ > 0.0 ? bp : (nn_ < 0.0 ? bn : 0.0);
-              const double d = __dsub_rn(b_new, b_old);
-              if (lane == k) {
-                bc = b_new;
-                dc = d;
+            double zpre = __shfl_sync(0xffffffffu, zc, 0);
+            double dprev = 0.0;
+            double cr0 = 0.0, cr1 = 0.0;
+            const double* gcp = Gd + lane;    // G[lane][k] at gcp[k * nb]
+            const double* gop = Go1 + lane;   // G[t+1 column lane][t column k] at gop[k * nb1]
+            const bool lane_on = lane < nb, lane_on1 = lane < nb1;
+            for (int k0 = 0; k0 < nb; k0 += 4) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int k = k0 + u;
+                const double2 p0 = *reinterpret_cast<const double2*>(sprm + 4 * k);      // beta, 1/denom
+                const double2 p1 = *reinterpret_cast<const double2*>(sprm + 4 * k + 2);  // denom, G[k][k-1]
+                const bool kin = k < nb;
+                const double gcol = (kin && lane_on) ? gcp[k * nb] : 0.0;
+                const double gnx = (kin && lane_on1) ? gop[k * nb1] : 0.0;
+                const double zpre_n = __shfl_sync(0xffffffffu, zc, (k + 1) & 31);
+                const double z = fma(-dprev, p1.y, zpre);
+                const double np_ = __dsub_rn(z, lam1), nn_ = __dadd_rn(z, lam1);
+                const double qp = __dmul_rn(np_, p0.y), qn = __dmul_rn(nn_, p0.y);
+                const double bp = fma(fma(-qp, p1.x, np_), p0.y, qp);
+                const double bn = fma(fma(-qn, p1.x, nn_), p0.y, qn);
+                const double b_new = np_ > 0.0 ? bp : (nn_ < 0.0 ? bn : 0.0);
+                const double d = __dsub_rn(b_new, p0.x);
+                zc = fma(-d, gcol, zc);
+                if (u & 1) cr1 = fma(d, gnx, cr1);
+                else cr0 = fma(d, gnx, cr0);
+                if (lane == k) {
+                  bc = b_new;
+                  dc = d;
+                }
+                const double ad = fabs(d);
+                max_delta = ad > max_delta ? ad : max_delta;
+                dprev = d;
+                zpre = zpre_n;
               }
-              const double gk = (lane < nb) ? Gd[k * nb + lane] : 0.0;  // G symmetric: column k
-              zdot = fma(-d, gk, zdot);
-              const double ad = fabs(d);
-              max_delta = ad > max_delta ? ad : max_delta;
             }
-            // steps by column (solver's correction next step) and compacted to the
-            // nonzero ones for the workers' AXPY (d == 0 leaves r unchanged)
+            corr = cr0 + cr1;
+            PROF_LAP(3)
+            // steps by column (solver's correction next step), and per worker warp the
+            // list of the nonzero steps whose column run meets that warp's rows (tiles
+            // RPT w .. RPT w + RPT - 1), in column order (d == 0 leaves r unchanged)
             dfull[32 * (t & 1) + lane] = (lane < nb) ? dc : 0.0;
             {
-              const unsigned nzm = __ballot_sync(0xffffffffu, lane < nb && dc != 0.0);
-              if (lane < nb && dc != 0.0) {
-                const int pos = __popc(nzm & ((1u << lane) - 1u));
-                dd[32 * (t & 1) + pos] = dc;
-                nzi[32 * (t & 1) + pos] = lane;
+              const int a0 = (pkc >> 16) & 0xff, la = (pkc >> 24) & 0xff;
+              const bool nz = lane < nb && dc != 0.0 && la > 0;
+              const int wlo = a0 / RPT, whi = (a0 + la - 1) / RPT;
+              const unsigned lt = (1u << lane) - 1u;
+              int* const lc = lcp + (t & 1) * NWK * LCAP;
+              double* const lv = ldv + (t & 1) * NWK * LCAP;
+#pragma unroll
+              for (int w = 0; w < NWK; ++w) {
+                const bool mine = nz && wlo <= w && w <= whi;
+                const unsigned m = __ballot_sync(0xffffffffu, mine);
+                if (mine) {
+                  const int pos = __popc(m & lt);
+                  lc[w * LCAP + pos] = pkc;
+                  lv[w * LCAP + pos] = dc;
+                }
+                if (lane == 0) lcnt[(t & 1) * NWK + w] = __popc(m);
               }
-              if (lane == 0) enz[t & 1] = __popc(nzm);
             }
             if (lane < nb) {
               betas[bk.j0 + lane] = bc;
@@ -505,10 +629,10 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
               acc_max = fmax(acc_max, ab);
             }
             int stop = 0;
-            if (b == nblk - 1) {  // sweep complete: the reference's stop rule (elastic_net.py:158)
+            if (bcur == nblk - 1) {  // sweep complete: the reference's stop rule (elastic_net.py:158)
               const double l1 = warp_sum(acc_l1), l2 = warp_sum(acc_l2), mabs = warp_max(acc_max);
               const double md = warp_max(max_delta);
-              const int sw = static_cast<int>(t / nblk);
+              const int sw = swc;
               const bool cv = md <= __dmul_rn(tol, fmax(mabs, 1.0));
               if (lane == 0) {
                 red[8 + 2 * (sw & 1)] = l1;
@@ -520,46 +644,53 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
               max_delta = acc_l1 = acc_l2 = acc_max = 0.0;
             }
             if (lane == 0) ctl[2 + (t & 1)] = stop;
+            PROF_LAP(4)
           } else if (lane == 0) {
             ctl[2 + (t & 1)] = 1;
           }
-        } else {
+        } else if (worker) {
           // workers: r -= W_{t-1} d_{t-1}, then (unless stopped) the dots of t+1
           if (t > 0) {
             const uint32_t e = t - 1;
-            axpy_nz(slot_of(e), dd + 32 * (e & 1), nzi + 32 * (e & 1), enz[e & 1], par + 32 * (e & 3));
+            const int li = (e & 1) * NWK + (warp - 1);
+            axpy_cols(slot_of(e), ldv + li * LCAP, lcp + li * LCAP, lcnt[li]);
           }
-          if (warp == NWK && !stopped && t + 2 < total) {
-            publish((t + 2) & 3);                             // packed at step t-1
-            pack_raw();                                       // element t+3 (raw loads of step t-1)
-            if (t + 4 < total) pfetch_d(pd);                  // element t+4's columns (descriptor of step t-1)
-            if (t + 5 < total) pd = blk[(t + 5) % nblk];      // element t+5's descriptor
-          }
+          PROF_LAP(0)
+          PROF_LAP(1)
           worker_bar();  // rs current, parameters of t+2 published
+          PROF_LAP(2)
           if (!stopped && t + 1 < total) {
             const uint32_t e = t + 1;
             wait_next();
-            const double* Wb = slot_of(e);
-            const int* pk = par + 32 * (e & 3);
-            for (int j = warp - 1; j < enb[e & 3]; j += NWK) {
-              const double z = col_dot(Wb, pk[j], false);
-              if (lane == 0) zraw[32 * (e & 1) + j] = z;
-            }
+            PROF_LAP(4)
+            block_dots(slot_of(e), par + 32 * (e & 3), enb[e & 3], zraw + 32 * (e & 1));
           }
-          if (t > 0 && (t - 1) % nblk == static_cast<uint32_t>(nblk - 1)) {
-            // the AXPY above completed sweep sw: its residual sum of squares
-            const int sw = static_cast<int>((t - 1) / nblk);
-            double rr = fma(r[0], r[0], fma(r[1], r[1], fma(r[2], r[2], r[3] * r[3])));
+          PROF_LAP(3)
+          if (sweep_closed) {
+            // the AXPY above completed sweep swc - 1: its residual sum of squares
+            const int sw = swc - 1;
+            double rr = 0.0;
+#pragma unroll
+            for (int k = 0; k < RPT; ++k) rr = fma(r[k], r[k], rr);
             rr = warp_sum(rr);
-            if (lane == 0) red[16 + 8 * (sw & 1) + warp - 1] = rr;
+            if (lane == 0) red[32 + 16 * (sw & 1) + warp - 1] = rr;
           }
         }
+        else if (!stopped && t + 2 < total) {
+          // stream warp: the parameter pipeline (global loads; nothing else waits on them)
+          publish((t + 2) & 3);                             // packed at step t-1
+          pack_raw();                                       // element t+3 (raw loads of step t-1)
+          if (t + 4 < total) pfetch_d(pd);                  // element t+4's columns (descriptor of step t-1)
+          if (t + 5 < total) pd = blk[modn(bcur + 5)];      // element t+5's descriptor
+        }
+        PROF_LAP(5)
         cta_bar();  // end of step t
-        if (t > 0 && (t - 1) % nblk == static_cast<uint32_t>(nblk - 1) && tid == 32) {
-          const int sw = static_cast<int>((t - 1) / nblk);
+        PROF_LAP(6)
+        if (sweep_closed && tid == DT) {
+          const int sw = swc - 1;
           double rss = 0.0;
 #pragma unroll
-          for (int w = 0; w < NWK; ++w) rss += red[16 + 8 * (sw & 1) + w];
+          for (int w = 0; w < NWK; ++w) rss += red[32 + 16 * (sw & 1) + w];
           const double obj = __dadd_rn(__dadd_rn(__dmul_rn(0.5, rss), __dmul_rn(lam1, red[8 + 2 * (sw & 1)])),
                                        __dmul_rn(__dmul_rn(0.5, lam2), red[9 + 2 * (sw & 1)]));
           if (a.hist != nullptr) a.hist[a.hist_off[s] + sw] = obj;
@@ -567,14 +698,28 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
         }
         if (stopped) break;  // this was the drain step (the final AXPY)
         if (q < total && ctl[2 + (t & 1)] == 0) {  // refill the slot of element t-1
-          issue(q, true, static_cast<int>((q + 1) % nblk));
+          const int qn = modn(qb + 1);
+          issue(q, true, qn);
+          qb = qn;
           ++q;
         }
+        if (++bcur == nblk) {
+          bcur = 0;
+          ++swc;
+        }
+        PROF_LAP(7)
       }
+#ifdef PAM_BLK_PROF
+      if (blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == 1 || warp == NWK || warp == NWK + 1))
+        printf("blkprof fit %d warp %d nblk %d M %d: %lld %lld %lld %lld %lld %lld %lld %lld\n", (int)s, warp, nblk, M, pf_t[0], pf_t[1], pf_t[2], pf_t[3], pf_t[4], pf_t[5], pf_t[6], pf_t[7]);
+#endif
       if (max_iters == 0) {
         // objective at the given beta (prologue residual)
         double rr = 0.0, q1 = 0.0, q2 = 0.0;
-        if (!solver) rr = fma(r[0], r[0], fma(r[1], r[1], fma(r[2], r[2], r[3] * r[3])));
+        if (worker) {
+#pragma unroll
+          for (int k = 0; k < RPT; ++k) rr = fma(r[k], r[k], rr);
+        }
         for (int j = tid; j < M; j += NT) {
           const double bj = betas[j];
           q1 += fabs(bj);
@@ -584,22 +729,23 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
         q1 = warp_sum(q1);
         q2 = warp_sum(q2);
         if (lane == 0) {
-          zraw[warp] = rr;
-          zraw[16 + warp] = q1;
-          dd[warp] = q2;
+          red[warp] = rr;
+          red[20 + warp] = q1;
+          red[40 + warp] = q2;
         }
         cta_bar();
         if (tid == 32) {
           double rss = 0.0, t1 = 0.0, t2 = 0.0;
-          for (int w = 0; w < NWK + 1; ++w) {
-            rss += zraw[w];
-            t1 += zraw[16 + w];
-            t2 += dd[w];
+          for (int w = 0; w < NWK + 2; ++w) {
+            rss += red[w];
+            t1 += red[20 + w];
+            t2 += red[40 + w];
           }
           red[12] = __dadd_rn(__dadd_rn(__dmul_rn(0.5, rss), __dmul_rn(lam1, t1)), __dmul_rn(__dmul_rn(0.5, lam2), t2));
         }
       }
       // observe every element issued beyond the stop (at most STAGES - 1 behind)
+      if (streamer) seen = q;  // never waited in the sweeps; phases are derived from ebase + seen
       while (seen < q) wait_next();
       cta_bar();
       if (tid == 32) {
@@ -625,8 +771,8 @@ int64_t cd_block_workspace_bytes(int64_t S, int64_t total_slots) {
 template <int SLOT_WD, int GMAX, int MINB>
 int launch_block_pipe_cfg(const CdArgs& a, void* block_ws, cudaStream_t stream) {
   using namespace bp;
-  const size_t smem = static_cast<size_t>(STAGES) * (SLOT_WD + 2 * GMAX * GMAX) * 8 + (1024 + 64 * 3 + 32) * 8 +
-                      (128 + 4 + 64 + 2 + 10) * 4 + 8 * STAGES + 16;
+  const size_t smem = static_cast<size_t>(STAGES) * (SLOT_WD + 2 * GMAX * GMAX) * 8 + (1024 + 64 * 4 + 2 * NWK * LCAP) * 8 +
+                      (128 + 4 + 2 * NWK * LCAP + 2 * NWK + 10) * 4 + 8 * STAGES + 16;
   auto kernel = cd_block_kernel<SLOT_WD, GMAX, MINB>;
   PAM_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   PAM_CUDA_CHECK(cudaMemsetAsync(a.queue, 0, sizeof(unsigned), stream));
@@ -636,14 +782,13 @@ int launch_block_pipe_cfg(const CdArgs& a, void* block_ws, cudaStream_t stream) 
   return PAM_OK;
 }
 
-// <= 2 fits per SM: one CTA per SM (C3's 256 fits in two waves measured
-// faster than two CTAs per SM with half the slot), 4 x (44 KB W + 2 x 2 KB
-// Gram) slots, blocks of up to 16 columns (a BASELINE C2/C3 column is ~5 KB of
-// tiles, so the W slot decides); more fits: two CTAs per SM, 4 x (20 KB + 4 KB).
+// One CTA per SM (544 threads; C3's 256 fits run in two waves, which measured
+// faster than two CTAs per SM with half the slot), 4 x (44 KB W + 2 x 2 KB Gram)
+// slots, blocks of up to 16 columns (a BASELINE C2/C3 column is ~5 KB of tiles,
+// so the W slot decides the block size in round 0).
 int launch_cd_block(const CdArgs& a, int max_rows, void* block_ws, cudaStream_t stream) {
   if (max_rows > 1024 || block_ws == nullptr) return PAM_ERR_UNSUPPORTED;
-  if (a.S <= 2 * sm_count()) return launch_block_pipe_cfg<5632, 16, 1>(a, block_ws, stream);
-  return launch_block_pipe_cfg<2560, 16, 2>(a, block_ws, stream);
+  return launch_block_pipe_cfg<5632, 16, 1>(a, block_ws, stream);
 }
 
 }  // namespace pam

@@ -29,7 +29,11 @@ def main():
     ap.add_argument("--iters", type=int, default=300)
     ap.add_argument("--rounds", type=int, default=1)
     ap.add_argument("--repeat", type=int, default=1)
+    ap.add_argument("--lib", default=None, help="alternative libpam_b200.so build (A/B of kernel variants)")
     args = ap.parse_args()
+    if args.lib:
+        from paper_2605_16564_b200 import _native
+        _native.LIB_PATH = Path(args.lib).resolve()
     E.set_options(cd_form=args.form, cd_kernel=args.kernel)
     wl = {"C2": workloads.config2, "C3": workloads.config3,
           "C4": lambda: workloads.config4(with_refined_eval=False)}[args.config]()
