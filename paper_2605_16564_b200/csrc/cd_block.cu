@@ -85,8 +85,8 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
   double* const ldv = zraw + 64;                // [2][NWK][LCAP] nonzero block steps, per worker warp
   double* const dfull = ldv + 2 * NWK * LCAP;   // [2][32] block steps by column (solver)
   double* const red = dfull + 64;               // [64] reductions (sweep-parity double-buffered)
-  double* const sprm = red + 64;                // [16][4] solver: {beta, 1/denom, denom, G[k][k-1]} of column k
-  int* const par = reinterpret_cast<int*>(sprm + 64);  // [4][32] packed column parameters (element & 3)
+  double* const sprm = red + 64;                // [20][4] solver: {beta, 1/denom, G[k][k-1], G[k][k-2]} of column k
+  int* const par = reinterpret_cast<int*>(sprm + 80);  // [4][32] packed column parameters (element & 3)
   int* const enb = par + 128;                         // [4] columns of element (e & 3)
   int* const lcp = enb + 4;                           // [2][NWK][LCAP] packed parameters of the listed columns
   int* const lcnt = lcp + 2 * NWK * LCAP;             // [2][NWK] entries of each worker warp's list
@@ -190,7 +190,10 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
       // ---- the ring: element e (counted from the pass start) = one block's packed
       //      W + its Gram blocks; thread 32 issues, every thread waits each element
       //      once, in order (`seen`), so no wait ever lags a slot by two phases
-      Blk ibk;  // thread 32: descriptor of its next issue (loaded one issue ahead)
+#ifdef PAM_BLK_PROF_TMA
+      long long tma_cyc = 0, tma_bytes = 0;
+#endif
+      Blk ibk;  // stream thread: descriptor of its next issue (loaded one issue ahead)
       auto iload = [&](int b) {
         if (tid == DT) ibk = blk[b];
       };
@@ -206,13 +209,25 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
           bulk_g2s(slots_s + st * (SLOT_D * 8), Ws + bk.woff, wbytes, bar);
           if (gbytes) bulk_g2s(slots_s + (st * SLOT_D + SLOT_WD) * 8, Gf + bk.gd, gbytes, bar);
           if (obytes) bulk_g2s(slots_s + (st * SLOT_D + SLOT_WD + GD) * 8, Gf + bk.go, obytes, bar);
+#ifdef PAM_BLK_PROF_TMA
+          {
+            const long long c0 = clock64();
+            while (!mbar_test_s(bar, ((ebase + e) / STAGES) & 1u)) {
+            }
+            tma_cyc += clock64() - c0;
+            tma_bytes += wbytes + gbytes + obytes;
+          }
+#endif
         }
         iload(b_next);
       };
       auto slot_of = [&](uint32_t e) -> const double* { return slots + ((ebase + e) % STAGES) * SLOT_D; };
       uint32_t seen = 0;
+      // one lane polls, the warp follows through __syncwarp (a warp-wide try_wait on
+      // one barrier word from nine warps at once measured ~700 cycles per step)
       auto wait_next = [&]() {
-        mbar_wait_s(bars_s + ((ebase + seen) % STAGES) * 8, ((ebase + seen) / STAGES) & 1u);
+        if (lane == 0) mbar_wait_s(bars_s + ((ebase + seen) % STAGES) * 8, ((ebase + seen) / STAGES) & 1u);
+        __syncwarp();
         ++seen;
       };
       // packed column parameters of block b: registers (one warp, lane c <-> column
@@ -291,25 +306,33 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
         const int n2 = 16 * la;  // double2 elements of the run
         const int step = 32 * nh;
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0, s5 = 0.0, s6 = 0.0, s7 = 0.0;
-        int i = lane + 32 * h;
-        for (; i + 3 * step < n2; i += 4 * step) {  // four independent element pairs per lane per pass
-          const double2 wa = w2[i], wb = w2[i + step], wc = w2[i + 2 * step], wd = w2[i + 3 * step];
-          const double2 xa = self ? wa : x2[i], xb = self ? wb : x2[i + step];
-          const double2 xc = self ? wc : x2[i + 2 * step], xd = self ? wd : x2[i + 3 * step];
-          s0 = fma(wa.x, xa.x, s0);
-          s1 = fma(wa.y, xa.y, s1);
-          s2 = fma(wb.x, xb.x, s2);
-          s3 = fma(wb.y, xb.y, s3);
-          s4 = fma(wc.x, xc.x, s4);
-          s5 = fma(wc.y, xc.y, s5);
-          s6 = fma(wd.x, xd.x, s6);
-          s7 = fma(wd.y, xd.y, s7);
-        }
-        for (; i < n2; i += step) {
-          const double2 wa = w2[i];
-          const double2 xa = self ? wa : x2[i];
-          s0 = fma(wa.x, xa.x, s0);
-          s1 = fma(wa.y, xa.y, s1);
+        const double2 zz = make_double2(0.0, 0.0);
+        // passes of eight element pairs per lane, every load of a pass issued before
+        // its FMAs (pairs past the run read as zero); a BASELINE C2/C3 column is one pass
+        for (int i = lane + 32 * h; i < n2; i += 8 * step) {
+          double2 wv[8], xv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const bool in = i + u * step < n2;
+            wv[u] = in ? w2[i + u * step] : zz;
+            xv[u] = self ? wv[u] : (in ? x2[i + u * step] : zz);
+          }
+          s0 = fma(wv[0].x, xv[0].x, s0);
+          s1 = fma(wv[0].y, xv[0].y, s1);
+          s2 = fma(wv[1].x, xv[1].x, s2);
+          s3 = fma(wv[1].y, xv[1].y, s3);
+          s4 = fma(wv[2].x, xv[2].x, s4);
+          s5 = fma(wv[2].y, xv[2].y, s5);
+          s6 = fma(wv[3].x, xv[3].x, s6);
+          s7 = fma(wv[3].y, xv[3].y, s7);
+          s0 = fma(wv[4].x, xv[4].x, s0);
+          s1 = fma(wv[4].y, xv[4].y, s1);
+          s2 = fma(wv[5].x, xv[5].x, s2);
+          s3 = fma(wv[5].y, xv[5].y, s3);
+          s4 = fma(wv[6].x, xv[6].x, s4);
+          s5 = fma(wv[6].y, xv[6].y, s5);
+          s6 = fma(wv[7].x, xv[7].x, s6);
+          s7 = fma(wv[7].y, xv[7].y, s7);
         }
         return warp_sum(((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7)));
       };
@@ -502,6 +525,10 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
       }
       double max_delta = 0.0, acc_l1 = 0.0, acc_l2 = 0.0, acc_max = 0.0;  // solver, per sweep
       double corr = 0.0;  // solver: G[t, t-1] d_{t-1} of this lane's column (accumulated during step t-1)
+      double invc = 0.0, ninv = 0.0;    // 1 / (col_sq + lam2) of this / the next block's column
+      double g1n = 0.0, g2n = 0.0;      // next block's G[c][c-1], G[c][c-2] (read from its slot a step early)
+      int pkn = 0;                      // next block's packed column parameters
+      bool first_blk = true;
       int bcur = 0, swc = 0;  // t % nblk, t / nblk
       PROF_DECL
       for (uint32_t t = 0; total > 0; ++t) {
@@ -517,9 +544,12 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
             if (nblk > 1 || t == 0) {
               bc = nbx;
               csc = ncs;
+              if (t == 0) {
+                const double dn0 = __dadd_rn(ncs, lam2);
+                ninv = dn0 > 0.0 ? __ddiv_rn(1.0, dn0) : 0.0;
+              }
+              invc = ninv;
             }
-            const double dnc = __dadd_rn(csc, lam2);
-            const double invc = dnc > 0.0 ? __ddiv_rn(1.0, dnc) : 0.0;
             if (nblk > 1 && t + 1 < total) sprefetch(sd_n1);  // its betas were written by this lane
             if (t + 2 < total) sd_n2 = blk[modn(bcur + 2)];
             PROF_LAP(0)
@@ -539,29 +569,44 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
             const double zdot = (lane < nb) ? __dsub_rn(zb[lane] + zb[16 + lane], corr) : 0.0;
             double zc = __dadd_rn(__dmul_rn(csc, bc), zdot);
             // per-column constants, broadcast-read inside the loop (columns >= nb:
-            // zeros, so a padded step is exactly d = 0)
+            // zeros, so a padded step is exactly d = 0): beta, 1 / (col_sq + lam2) and the
+            // two sub-diagonal Gram entries G[k][k-1], G[k][k-2] (loaded a step early
+            // from this block's slot, except for the first block)
             {
               const bool on = lane < nb;
-              const double gp = (on && lane > 0) ? Gd[(lane - 1) * nb + lane] : 0.0;  // G[lane][lane-1]
-              if (lane < 16) {
+              double g1 = g1n, g2 = g2n;
+              int pk0 = pkn;
+              if (first_blk) {
+                g1 = (on && lane > 0) ? Gd[(lane - 1) * nb + lane] : 0.0;
+                g2 = (on && lane > 1) ? Gd[(lane - 2) * nb + lane] : 0.0;
+                pk0 = par[32 * (t & 3) + lane];
+                first_blk = false;
+              }
+              pkn = pk0;
+              if (lane < 20) {
                 double2* sp = reinterpret_cast<double2*>(sprm + 4 * lane);
                 sp[0] = make_double2(on ? bc : 0.0, on ? invc : 0.0);
-                sp[1] = make_double2(on ? dnc : 0.0, gp);
+                sp[1] = make_double2(g1, g2);
               }
             }
             __syncwarp();
             PROF_LAP(2)
             // the block's cyclic updates (elastic_net.py:137-156).  Lane c carries
-            // zc = col_sq_c beta_c + W_c . r with the block's earlier steps applied;
-            // column k's value is broadcast one step EARLY (before step k-1 is known)
-            // and step k-1's term -d_{k-1} G[k][k-1] is applied to the broadcast copy,
-            // so the shuffle is off the serial chain: per column the chain is one FMA,
-            // the soft threshold and the step difference.  Four columns per
-            // straight-line group (operand loads hoist above the chain).
-            const int pkc = par[32 * (t & 3) + lane];  // this lane's column parameters (for the AXPY lists)
+            // zc = col_sq_c beta_c + W_c . r with the block's earlier steps applied.
+            // Column k's value is broadcast TWO steps early (steps <= k-3 applied) and
+            // the terms of steps k-2 and k-1 are applied to the broadcast copy:
+            //   z_k = [zpre_k - d_{k-2} G[k][k-2] + beta_{k-1} G[k][k-1]] - b_{k-1} G[k][k-1]
+            // with b_{k-1} the NEW coefficient of column k-1, so the bracket is ready
+            // before b_{k-1} and the serial chain per column is one FMA, the shift by
+            // lam1, one multiply by 1 / (col_sq + lam2) and the sign selects.  (The
+            // quotient is the product with the correctly rounded reciprocal: <= 1.5 ulp
+            // from the reference's division, far inside the rounding class of the
+            // reordered inner products.)  Four columns per straight-line group.
+            const int pkc = pkn;  // this lane's column parameters (for the AXPY lists)
             double dc = 0.0;
-            double zpre = __shfl_sync(0xffffffffu, zc, 0);
-            double dprev = 0.0;
+            double zq = __shfl_sync(0xffffffffu, zc, 0);    // bracket of column k
+            double zp1 = __shfl_sync(0xffffffffu, zc, 1);   // broadcast copy of column k+1 (steps <= k-2)
+            double bprev = 0.0, dprev = 0.0;
             double cr0 = 0.0, cr1 = 0.0;
             const double* gcp = Gd + lane;    // G[lane][k] at gcp[k * nb]
             const double* gop = Go1 + lane;   // G[t+1 column lane][t column k] at gop[k * nb1]
@@ -570,18 +615,22 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const int k = k0 + u;
-                const double2 p0 = *reinterpret_cast<const double2*>(sprm + 4 * k);      // beta, 1/denom
-                const double2 p1 = *reinterpret_cast<const double2*>(sprm + 4 * k + 2);  // denom, G[k][k-1]
+                const double2 p0 = *reinterpret_cast<const double2*>(sprm + 4 * k);        // beta_k, inv_k
+                const double2 p1 = *reinterpret_cast<const double2*>(sprm + 4 * k + 2);    // G[k][k-1], G[k][k-2]
+                const double2 q1 = *reinterpret_cast<const double2*>(sprm + 4 * k + 6);    // G[k+1][k], G[k+1][k-1]
                 const bool kin = k < nb;
                 const double gcol = (kin && lane_on) ? gcp[k * nb] : 0.0;
                 const double gnx = (kin && lane_on1) ? gop[k * nb1] : 0.0;
-                const double zpre_n = __shfl_sync(0xffffffffu, zc, (k + 1) & 31);
-                const double z = fma(-dprev, p1.y, zpre);
+                // bracket of column k+1 from the copy taken one step ago (steps <= k-2
+                // applied): step k-1's term and column k's OLD coefficient times G[k+1][k]
+                const double zq_n = fma(p0.x, q1.x, fma(-dprev, q1.y, zp1));
+                const double zp2 = __shfl_sync(0xffffffffu, zc, (k + 2) & 31);  // steps <= k-1 applied
+                // serial chain
+                const double z = fma(-bprev, p1.x, zq);
                 const double np_ = __dsub_rn(z, lam1), nn_ = __dadd_rn(z, lam1);
                 const double qp = __dmul_rn(np_, p0.y), qn = __dmul_rn(nn_, p0.y);
-                const double bp = fma(fma(-qp, p1.x, np_), p0.y, qp);
-                const double bn = fma(fma(-qn, p1.x, nn_), p0.y, qn);
-                const double b_new = np_ > 0.0 ? bp : (nn_ < 0.0 ? bn : 0.0);
+                const double b_new = np_ > 0.0 ? qp : (nn_ < 0.0 ? qn : 0.0);
+                // off the chain
                 const double d = __dsub_rn(b_new, p0.x);
                 zc = fma(-d, gcol, zc);
                 if (u & 1) cr1 = fma(d, gnx, cr1);
@@ -592,16 +641,31 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
                 }
                 const double ad = fabs(d);
                 max_delta = ad > max_delta ? ad : max_delta;
+                bprev = b_new;
                 dprev = d;
-                zpre = zpre_n;
+                zq = zq_n;
+                zp1 = zp2;
               }
             }
             corr = cr0 + cr1;
+            // next block: its sub-diagonal Gram entries and column parameters (slot t+1 is
+            // resident, parameters published two steps ago) and 1 / (col_sq + lam2) of the
+            // col_sq prefetched at the top of this step -- all off the next step's chain
+            if (has_next) {
+              const double* Gd1 = slot_of(t + 1) + SLOT_WD;
+              const bool on1 = lane < nb1;
+              g1n = (on1 && lane > 0) ? Gd1[(lane - 1) * nb1 + lane] : 0.0;
+              g2n = (on1 && lane > 1) ? Gd1[(lane - 2) * nb1 + lane] : 0.0;
+              pkn = par[32 * ((t + 1) & 3) + lane];
+              if (nblk > 1) {
+                const double dn1 = __dadd_rn(ncs, lam2);
+                ninv = dn1 > 0.0 ? __ddiv_rn(1.0, dn1) : 0.0;
+              }
+            }
             PROF_LAP(3)
             // steps by column (solver's correction next step), and per worker warp the
             // list of the nonzero steps whose column run meets that warp's rows (tiles
             // RPT w .. RPT w + RPT - 1), in column order (d == 0 leaves r unchanged)
-            dfull[32 * (t & 1) + lane] = (lane < nb) ? dc : 0.0;
             {
               const int a0 = (pkc >> 16) & 0xff, la = (pkc >> 24) & 0xff;
               const bool nz = lane < nb && dc != 0.0 && la > 0;
@@ -709,6 +773,9 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
         }
         PROF_LAP(7)
       }
+#ifdef PAM_BLK_PROF_TMA
+      if (blockIdx.x == 0 && tid == DT) printf("tma fit %d: %lld cycles for %lld bytes, %u issues\n", (int)s, tma_cyc, tma_bytes, q);
+#endif
 #ifdef PAM_BLK_PROF
       if (blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == 1 || warp == NWK || warp == NWK + 1))
         printf("blkprof fit %d warp %d nblk %d M %d: %lld %lld %lld %lld %lld %lld %lld %lld\n", (int)s, warp, nblk, M, pf_t[0], pf_t[1], pf_t[2], pf_t[3], pf_t[4], pf_t[5], pf_t[6], pf_t[7]);
@@ -771,7 +838,7 @@ int64_t cd_block_workspace_bytes(int64_t S, int64_t total_slots) {
 template <int SLOT_WD, int GMAX, int MINB>
 int launch_block_pipe_cfg(const CdArgs& a, void* block_ws, cudaStream_t stream) {
   using namespace bp;
-  const size_t smem = static_cast<size_t>(STAGES) * (SLOT_WD + 2 * GMAX * GMAX) * 8 + (1024 + 64 * 4 + 2 * NWK * LCAP) * 8 +
+  const size_t smem = static_cast<size_t>(STAGES) * (SLOT_WD + 2 * GMAX * GMAX) * 8 + (1024 + 64 * 3 + 80 + 2 * NWK * LCAP) * 8 +
                       (128 + 4 + 2 * NWK * LCAP + 2 * NWK + 10) * 4 + 8 * STAGES + 16;
   auto kernel = cd_block_kernel<SLOT_WD, GMAX, MINB>;
   PAM_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

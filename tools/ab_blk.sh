@@ -1,5 +1,5 @@
 V=paper_2605_16564_b200/build/variants
-timeout 120 python tools/cd_probe.py C2 --rounds 1 --kernel block --iters 400 --lib $V/libpam_prof.so 2>&1 | grep -E "blkprof|cd_s" | tail -4
+timeout 120 python tools/cd_probe.py C2 --rounds 1 --kernel block --iters 400 --lib $V/libpam_prof.so 2>&1 | grep -E "blkprof|cd_s" | tail -5
 for cfg in "C2 --rounds 1" "C2 --rounds 3" "C3 --rounds 2"; do
 for lib in old cur; do
   if [ $lib = cur ]; then L=""; else L="--lib $V/libpam_$lib.so"; fi
