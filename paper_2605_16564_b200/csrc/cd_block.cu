@@ -80,8 +80,8 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
   constexpr int SLOT_D = SLOT_WD + 2 * GD;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* const slots = reinterpret_cast<double*>(smem_raw);
-  double* const rs = slots + STAGES * SLOT_D;  // [1024] residual mirror (position order)
-  double* const zraw = rs + 1024;               // [2][2][16] block dots (element parity, run half, column)
+  double* const zpart = slots + STAGES * SLOT_D;  // [2][NWK][16] block dots per worker warp (element parity)
+  double* const zraw = zpart + 2 * NWK * 16;      // [64] staging (beta0 of a prologue block)
   double* const ldv = zraw + 64;                // [2][NWK][LCAP] nonzero block steps, per worker warp
   double* const dfull = ldv + 2 * NWK * LCAP;   // [2][32] block steps by column (solver)
   double* const red = dfull + 64;               // [64] reductions (sweep-parity double-buffered)
@@ -110,7 +110,6 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
   unsigned item = blockIdx.x;
 
   auto cta_bar = [&]() { __syncthreads(); };
-  auto worker_bar = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(NWK * 32) : "memory"); };
 
   while (item < a.S) {
     const int64_t s = a.order ? a.order[item] : static_cast<int64_t>(item);
@@ -171,17 +170,18 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
           ctl[0] = nb;
         }
       }
-      // residual rows RPT wt .. (workers; position order, perm -> local row)
+      // residual rows of a worker thread (position order, perm -> local row): worker warp w
+      // owns positions [32 RPT w, 32 RPT (w + 1)); lane l the pairs 64 v + 2 l + {0, 1}, so a
+      // warp's 16-byte tile loads are contiguous in shared memory (no bank conflicts)
       double r[RPT];
 #pragma unroll
       for (int k = 0; k < RPT; ++k) r[k] = 0.0;
       if (worker) {
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
-          const int p = RPT * wt + k;
+          const int p = 32 * RPT * (warp - 1) + 64 * (k >> 1) + 2 * lane + (k & 1);
           const int row = a.perm ? (p < N ? a.perm[r0 + p] : 0) : p;
           r[k] = (p < N) ? a.y[r0 + row] : 0.0;
-          rs[p] = r[k];
         }
       }
       cta_bar();
@@ -265,8 +265,9 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
       // the FMAs; a column outside this thread's tile, or past cnt, contributes an
       // exact zero step), in ascending k
       auto axpy_cols = [&](const double* Wb, const double* dv, const int* cpv, int cnt) {
-        const int tile = (RPT * wt) >> 5;
-        const int sub = (RPT * wt) & 31;
+        const int tile0 = RPT * (warp - 1) + (lane >> 4);  // tile of pair v: tile0 + 2 v
+        const int sub = (2 * lane) & 31;
+        const double2 zz = make_double2(0.0, 0.0);
         for (int k = 0; k < cnt; k += 4) {
           double d[4];
           double2 w[4][RPT / 2];
@@ -276,11 +277,13 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
             const int kk = ok ? k + u : k;
             const int cp = cpv[kk];
             const int o = cp & 0xffff, a0 = (cp >> 16) & 0xff, la = cp >> 24;
-            const bool in = ok && static_cast<unsigned>(tile - a0) < static_cast<unsigned>(la);
-            const double2* w2 = reinterpret_cast<const double2*>(Wb + (in ? o + 32 * (tile - a0) + sub : 0));
 #pragma unroll
-            for (int v = 0; v < RPT / 2; ++v) w[u][v] = w2[v];
-            d[u] = in ? dv[kk] : 0.0;
+            for (int v = 0; v < RPT / 2; ++v) {
+              const int tr = tile0 + 2 * v - a0;
+              const bool in = ok && static_cast<unsigned>(tr) < static_cast<unsigned>(la);
+              w[u][v] = in ? *reinterpret_cast<const double2*>(Wb + o + 32 * tr + sub) : zz;
+            }
+            d[u] = dv[kk];
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -291,113 +294,89 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
             }
           }
         }
-        double2* r2 = reinterpret_cast<double2*>(rs + RPT * wt);
-#pragma unroll
-        for (int v = 0; v < RPT / 2; ++v) r2[v] = make_double2(r[2 * v], r[2 * v + 1]);
       };
-      // a warp's dot of packed column cp with rs (self: with itself) -> every lane.
-      // The run's double2 elements are taken in chunks of 32 (one per lane); with
-      // nh == 2 this warp takes the chunks of parity h (the other half goes to a
-      // second warp and the two partial sums are added by the consumer).
-      auto col_dot = [&](const double* Wb, int cp, bool self, int h, int nh) -> double {
-        const int o = cp & 0xffff, a0 = (cp >> 16) & 0xff, la = cp >> 24;
+      // a warp's squared norm of packed column cp -> every lane (prologue col_sq)
+      auto col_sq_dot = [&](const double* Wb, int cp) -> double {
+        const int o = cp & 0xffff, la = cp >> 24;
         const double2* w2 = reinterpret_cast<const double2*>(Wb + o);
-        const double2* x2 = reinterpret_cast<const double2*>(rs + 32 * a0);
         const int n2 = 16 * la;  // double2 elements of the run
-        const int step = 32 * nh;
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0, s5 = 0.0, s6 = 0.0, s7 = 0.0;
-        const double2 zz = make_double2(0.0, 0.0);
-        // passes of eight element pairs per lane, every load of a pass issued before
-        // its FMAs (pairs past the run read as zero); a BASELINE C2/C3 column is one pass
-        for (int i = lane + 32 * h; i < n2; i += 8 * step) {
-          double2 wv[8], xv[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const bool in = i + u * step < n2;
-            wv[u] = in ? w2[i + u * step] : zz;
-            xv[u] = self ? wv[u] : (in ? x2[i + u * step] : zz);
-          }
-          s0 = fma(wv[0].x, xv[0].x, s0);
-          s1 = fma(wv[0].y, xv[0].y, s1);
-          s2 = fma(wv[1].x, xv[1].x, s2);
-          s3 = fma(wv[1].y, xv[1].y, s3);
-          s4 = fma(wv[2].x, xv[2].x, s4);
-          s5 = fma(wv[2].y, xv[2].y, s5);
-          s6 = fma(wv[3].x, xv[3].x, s6);
-          s7 = fma(wv[3].y, xv[3].y, s7);
-          s0 = fma(wv[4].x, xv[4].x, s0);
-          s1 = fma(wv[4].y, xv[4].y, s1);
-          s2 = fma(wv[5].x, xv[5].x, s2);
-          s3 = fma(wv[5].y, xv[5].y, s3);
-          s4 = fma(wv[6].x, xv[6].x, s4);
-          s5 = fma(wv[6].y, xv[6].y, s5);
-          s6 = fma(wv[7].x, xv[7].x, s6);
-          s7 = fma(wv[7].y, xv[7].y, s7);
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int i = lane;
+        for (; i + 32 < n2; i += 64) {
+          const double2 wa = w2[i], wb = w2[i + 32];
+          s0 = fma(wa.x, wa.x, s0);
+          s1 = fma(wa.y, wa.y, s1);
+          s2 = fma(wb.x, wb.x, s2);
+          s3 = fma(wb.y, wb.y, s3);
         }
-        return warp_sum(((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7)));
+        if (i < n2) {
+          const double2 wa = w2[i];
+          s0 = fma(wa.x, wa.x, s0);
+          s1 = fma(wa.y, wa.y, s1);
+        }
+        return warp_sum((s0 + s1) + (s2 + s3));
       };
-      // two columns at once (one warp): both columns' loads and reductions interleave
-      auto col_dot2 = [&](const double* Wb, int cpa, int cpb, double& za, double& zb2) {
-        const int oa = cpa & 0xffff, aa = (cpa >> 16) & 0xff, la_ = cpa >> 24;
-        const int ob = cpb & 0xffff, ab = (cpb >> 16) & 0xff, lb_ = cpb >> 24;
-        const double2* wa2 = reinterpret_cast<const double2*>(Wb + oa);
-        const double2* xa2 = reinterpret_cast<const double2*>(rs + 32 * aa);
-        const double2* wb2 = reinterpret_cast<const double2*>(Wb + ob);
-        const double2* xb2 = reinterpret_cast<const double2*>(rs + 32 * ab);
-        const int na = 16 * la_, nbb = 16 * lb_;
-        const int nmax = max(na, nbb);
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+      // workers: the dots of a block of nb <= 16 columns against the residual, ROW
+      // parallel: each thread multiplies its own rows (registers) with the columns'
+      // entries of those rows, the warp adds its 32 lanes' 16 partial sums by a
+      // halving butterfly (16 -> 8 -> 4 -> 2 -> 1 values per lane, then the last
+      // lane pair) and lanes 0, 2, .., 30 store the warp's 16 column sums to zp[16];
+      // the solver adds the worker warps' parts in warp order.  No residual mirror
+      // in shared memory: per block the shared-memory traffic is the block's tiles,
+      // once for the dots and once for the AXPY.
+      auto block_dots = [&](const double* Wb, const int* pk, int nb, double* zp) {
+        const int tile0 = RPT * (warp - 1) + (lane >> 4);  // tile of pair v: tile0 + 2 v
+        const int sub = (2 * lane) & 31;
         const double2 zz = make_double2(0.0, 0.0);
-        for (int i = lane; i < nmax; i += 64) {
-          const bool pa0 = i < na, pa1 = i + 32 < na, pb0 = i < nbb, pb1 = i + 32 < nbb;
-          const double2 w0 = pa0 ? wa2[i] : zz, w1 = pa1 ? wa2[i + 32] : zz;
-          const double2 v0 = pb0 ? wb2[i] : zz, v1 = pb1 ? wb2[i + 32] : zz;
-          const double2 x0 = pa0 ? xa2[i] : zz, x1 = pa1 ? xa2[i + 32] : zz;
-          const double2 y0 = pb0 ? xb2[i] : zz, y1 = pb1 ? xb2[i + 32] : zz;
-          a0 = fma(w0.x, x0.x, a0);
-          a1 = fma(w0.y, x0.y, a1);
-          a2 = fma(w1.x, x1.x, a2);
-          a3 = fma(w1.y, x1.y, a3);
-          b0 = fma(v0.x, y0.x, b0);
-          b1 = fma(v0.y, y0.y, b1);
-          b2 = fma(v1.x, y1.x, b2);
-          b3 = fma(v1.y, y1.y, b3);
-        }
-        double sa = (a0 + a1) + (a2 + a3), sb = (b0 + b1) + (b2 + b3);
+        double p[16];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          sa += __shfl_xor_sync(0xffffffffu, sa, o);
-          sb += __shfl_xor_sync(0xffffffffu, sb, o);
-        }
-        za = sa;
-        zb2 = sb;
-      };
-      // workers: the dots of a block of nb columns against rs -> zraw buffer zb
-      // ([2][16]: run half, column).  nb <= NWK / 2: two warps per column (run
-      // halves); nb <= NWK: one warp per column; more: columns w and w + NWK on
-      // warp w, interleaved.  Unsplit columns get a zero second half.
-      auto block_dots = [&](const double* Wb, const int* pk, int nb, double* zb) {
-        const int w = warp - 1;
-        if (nb <= NWK / 2) {
-          const int j = w % (NWK / 2), h = w / (NWK / 2);
-          if (j < nb) {
-            const double z = col_dot(Wb, pk[j], false, h, 2);
-            if (lane == 0) zb[16 * h + j] = z;
-          }
-        } else if (w < nb) {
-          double z0, z1 = 0.0;
-          const bool two = w + NWK < nb;
-          if (two) col_dot2(Wb, pk[w], pk[w + NWK], z0, z1);
-          else z0 = col_dot(Wb, pk[w], false, 0, 1);
-          if (lane == 0) {
-            zb[w] = z0;
-            zb[16 + w] = 0.0;
-            if (two) {
-              zb[w + NWK] = z1;
-              zb[16 + w + NWK] = 0.0;
+        for (int j0 = 0; j0 < 16; j0 += 4) {
+          if (j0 < nb) {
+            double2 w[4][RPT / 2];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int j = j0 + u;
+              const int cp = pk[j < nb ? j : j0];
+              const int o = cp & 0xffff, a0 = (cp >> 16) & 0xff, la = cp >> 24;
+#pragma unroll
+              for (int v = 0; v < RPT / 2; ++v) {
+                const int tr = tile0 + 2 * v - a0;
+                const bool in = j < nb && static_cast<unsigned>(tr) < static_cast<unsigned>(la);
+                w[u][v] = in ? *reinterpret_cast<const double2*>(Wb + o + 32 * tr + sub) : zz;
+              }
             }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+              for (int v = 0; v < RPT / 2; ++v) {
+                acc0 = fma(w[u][v].x, r[2 * v], acc0);
+                acc1 = fma(w[u][v].y, r[2 * v + 1], acc1);
+              }
+              p[j0 + u] = acc0 + acc1;
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) p[j0 + u] = 0.0;
           }
         }
+        // halving butterfly: after the level with lane bit b, a lane keeps the half
+        // of its values selected by that bit
+#pragma unroll
+        for (int lvl = 0; lvl < 4; ++lvl) {
+          const int half = 8 >> lvl;           // values kept after this level
+          const int bit = 16 >> lvl;           // lane bit of this level
+          const bool hi = (lane & bit) != 0;
+#pragma unroll
+          for (int i = 0; i < half; ++i) {
+            const double keep = hi ? p[i + half] : p[i];
+            const double send = hi ? p[i] : p[i + half];
+            p[i] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
+          }
+        }
+        const double tot = p[0] + __shfl_xor_sync(0xffffffffu, p[0], 1);
+        // value index held by this lane: bit 4 of the lane -> bit 3 of the index, ...
+        if ((lane & 1) == 0) zp[lane >> 1] = tot;
       };
       // ---- prologue pass: col_sq (elastic_net.py:85), r = y - W beta0 (94), and the
       //      diagonal and previous-block Gram blocks; elements 0..nblk-1, then block 0
@@ -424,7 +403,7 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
           const int* pk = par + 32 * (e & 3);
           if (!wrap) {
             for (int j = warp; j < nb; j += NWK + 2) {
-              const double cs = col_dot(Wb, pk[j], true, 0, 1);
+              const double cs = col_sq_dot(Wb, pk[j]);
               if (lane == 0) colsq[bk.j0 + j] = cs;
             }
           }
@@ -456,7 +435,7 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
           }
           if (!wrap && worker) axpy_cols(Wb, zraw, pk, nb);  // r -= W_b beta0_b
           asm volatile("fence.proxy.async.global;" ::: "memory");  // the sweeps re-read G by TMA
-          cta_bar();  // slot e-1 free, rs current
+          cta_bar();  // slot e-1 free
           if (q < np_el) {
             issue(q, false, pblock(q + 1 < np_el ? q + 1 : q));
             ++q;
@@ -505,7 +484,7 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
       cta_bar();
       if (worker && total > 0) {  // pre-step: dots of element 0 against the prologue residual
         wait_next();
-        block_dots(slot_of(0), par, enb[0], zraw);
+        block_dots(slot_of(0), par, enb[0], zpart + (warp - 1) * 16);
       }
       cta_bar();
 
@@ -529,6 +508,8 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
       double g1n = 0.0, g2n = 0.0;      // next block's G[c][c-1], G[c][c-2] (read from its slot a step early)
       int pkn = 0;                      // next block's packed column parameters
       bool first_blk = true;
+      int st_j = -1;      // deferred coefficient store: index (or -1) and value
+      double st_b = 0.0;
       int bcur = 0, swc = 0;  // t % nblk, t / nblk
       PROF_DECL
       for (uint32_t t = 0; total > 0; ++t) {
@@ -537,6 +518,8 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
         PROF_START
         if (solver) {
           if (!stopped) {
+            if (st_j >= 0) betas[st_j] = st_b;  // previous block's coefficients (deferred)
+            st_j = -1;
             sd_cur = sd_n1;
             sd_n1 = sd_n2;
             const Blk& bk = sd_cur;
@@ -565,8 +548,16 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
             const double* Go1 = slot_of(t + 1) + SLOT_WD + GD;
             const int nb1 = has_next ? sd_n1.nb : 0;
             // z = (zraw - G[t, t-1] d_{t-1}) + col_sq beta; lane c <-> column c
-            const double* zb = zraw + 32 * (t & 1);
-            const double zdot = (lane < nb) ? __dsub_rn(zb[lane] + zb[16 + lane], corr) : 0.0;
+            double zsum = 0.0;
+            if (lane < nb) {
+              const double* zb = zpart + (t & 1) * NWK * 16 + lane;
+              double zw[NWK];
+#pragma unroll
+              for (int w = 0; w < NWK; ++w) zw[w] = zb[16 * w];
+#pragma unroll
+              for (int w = 0; w < NWK; ++w) zsum += zw[w];  // worker warps in order
+            }
+            const double zdot = (lane < nb) ? __dsub_rn(zsum, corr) : 0.0;
             double zc = __dadd_rn(__dmul_rn(csc, bc), zdot);
             // per-column constants, broadcast-read inside the loop (columns >= nb:
             // zeros, so a padded step is exactly d = 0): beta, 1 / (col_sq + lam2) and the
@@ -685,8 +676,12 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
                 if (lane == 0) lcnt[(t & 1) * NWK + w] = __popc(m);
               }
             }
+            // the block's coefficients go to global memory at the top of the NEXT step:
+            // a store issued right before the CTA barrier holds every warp at the barrier
+            // until it is performed (~700 cycles per step, 40 % of all stall samples)
+            st_j = (lane < nb) ? bk.j0 + lane : -1;
+            st_b = bc;
             if (lane < nb) {
-              betas[bk.j0 + lane] = bc;
               const double ab = fabs(bc);
               acc_l1 += ab;
               acc_l2 = fma(bc, bc, acc_l2);
@@ -721,13 +716,11 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
           }
           PROF_LAP(0)
           PROF_LAP(1)
-          worker_bar();  // rs current, parameters of t+2 published
-          PROF_LAP(2)
           if (!stopped && t + 1 < total) {
             const uint32_t e = t + 1;
             wait_next();
             PROF_LAP(4)
-            block_dots(slot_of(e), par + 32 * (e & 3), enb[e & 3], zraw + 32 * (e & 1));
+            block_dots(slot_of(e), par + 32 * (e & 3), enb[e & 3], zpart + ((e & 1) * NWK + warp - 1) * 16);
           }
           PROF_LAP(3)
           if (sweep_closed) {
@@ -773,6 +766,7 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
         }
         PROF_LAP(7)
       }
+      if (solver && st_j >= 0) betas[st_j] = st_b;  // the last block's coefficients
 #ifdef PAM_BLK_PROF_TMA
       if (blockIdx.x == 0 && tid == DT) printf("tma fit %d: %lld cycles for %lld bytes, %u issues\n", (int)s, tma_cyc, tma_bytes, q);
 #endif
@@ -838,7 +832,7 @@ int64_t cd_block_workspace_bytes(int64_t S, int64_t total_slots) {
 template <int SLOT_WD, int GMAX, int MINB>
 int launch_block_pipe_cfg(const CdArgs& a, void* block_ws, cudaStream_t stream) {
   using namespace bp;
-  const size_t smem = static_cast<size_t>(STAGES) * (SLOT_WD + 2 * GMAX * GMAX) * 8 + (1024 + 64 * 3 + 80 + 2 * NWK * LCAP) * 8 +
+  const size_t smem = static_cast<size_t>(STAGES) * (SLOT_WD + 2 * GMAX * GMAX) * 8 + (2 * NWK * 16 + 64 * 3 + 80 + 2 * NWK * LCAP) * 8 +
                       (128 + 4 + 2 * NWK * LCAP + 2 * NWK + 10) * 4 + 8 * STAGES + 16;
   auto kernel = cd_block_kernel<SLOT_WD, GMAX, MINB>;
   PAM_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
