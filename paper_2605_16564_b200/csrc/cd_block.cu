@@ -58,8 +58,13 @@ constexpr int STAGES = 4;       // blocks t-1 (AXPY), t (solve), t+1 (dots), t+2
 #define PAM_BLK_NWK 8
 #endif
 constexpr int NWK = PAM_BLK_NWK;    // worker warps
-constexpr int NT = (NWK + 2) * 32;  // + solver warp 0 + stream warp NWK + 1
-constexpr int DT = (NWK + 1) * 32;  // the stream warp's issuing thread
+// Warp roles.  Warp w issues on scheduler w % 4: the solver (warp 0) keeps scheduler
+// 0 to itself -- its ~60-instruction serial stream per column gets every issue
+// slot -- sharing it only with the stream warp (4, a few instructions per step) and
+// an idle warp (8); the worker warps are the ones with w % 4 != 0.
+constexpr int NWARPS = NWK + 1 + (NWK + 2) / 3;  // NWK = 8: warps 0..10
+constexpr int NT = NWARPS * 32;
+constexpr int DT = 4 * 32;  // the stream warp's issuing thread
 constexpr int RPT = 1024 / (NWK * 32);  // residual rows per worker thread (= tiles per worker warp)
 static_assert(RPT == 2 || RPT == 4, "worker row ownership: two or four consecutive rows per thread");
 constexpr int LCAP = 16;            // entries per worker warp's AXPY list (= GMAX)
@@ -94,9 +99,9 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
   uint64_t* const bars = reinterpret_cast<uint64_t*>(ctl + 10);  // 8-byte aligned
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool solver = warp == 0;
-  const bool worker = warp >= 1 && warp <= NWK;
-  const bool streamer = warp == NWK + 1;  // descriptor / parameter pipeline and the bulk copies
-  const int wt = tid - 32;  // worker thread index, rows RPT wt .. RPT wt + RPT - 1
+  const int ww = warp - 1 - (warp >> 2);  // worker index of a worker warp
+  const bool worker = (warp & 3) != 0 && ww < NWK;
+  const bool streamer = warp == 4;  // descriptor / parameter pipeline and the bulk copies
   const uint32_t slots_s = smem_u32(slots);
   const uint32_t bars_s = smem_u32(bars);
 
@@ -179,7 +184,7 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
       if (worker) {
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
-          const int p = 32 * RPT * (warp - 1) + 64 * (k >> 1) + 2 * lane + (k & 1);
+          const int p = 32 * RPT * ww + 64 * (k >> 1) + 2 * lane + (k & 1);
           const int row = a.perm ? (p < N ? a.perm[r0 + p] : 0) : p;
           r[k] = (p < N) ? a.y[r0 + row] : 0.0;
         }
@@ -265,7 +270,7 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
       // the FMAs; a column outside this thread's tile, or past cnt, contributes an
       // exact zero step), in ascending k
       auto axpy_cols = [&](const double* Wb, const double* dv, const int* cpv, int cnt) {
-        const int tile0 = RPT * (warp - 1) + (lane >> 4);  // tile of pair v: tile0 + 2 v
+        const int tile0 = RPT * ww + (lane >> 4);  // tile of pair v: tile0 + 2 v
         const int sub = (2 * lane) & 31;
         const double2 zz = make_double2(0.0, 0.0);
         for (int k = 0; k < cnt; k += 4) {
@@ -325,7 +330,7 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
       // in shared memory: per block the shared-memory traffic is the block's tiles,
       // once for the dots and once for the AXPY.
       auto block_dots = [&](const double* Wb, const int* pk, int nb, double* zp) {
-        const int tile0 = RPT * (warp - 1) + (lane >> 4);  // tile of pair v: tile0 + 2 v
+        const int tile0 = RPT * ww + (lane >> 4);  // tile of pair v: tile0 + 2 v
         const int sub = (2 * lane) & 31;
         const double2 zz = make_double2(0.0, 0.0);
         double p[16];
@@ -402,7 +407,7 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
           const double* Wb = slot_of(e);
           const int* pk = par + 32 * (e & 3);
           if (!wrap) {
-            for (int j = warp; j < nb; j += NWK + 2) {
+            for (int j = warp; j < nb; j += NWARPS) {
               const double cs = col_sq_dot(Wb, pk[j]);
               if (lane == 0) colsq[bk.j0 + j] = cs;
             }
@@ -484,7 +489,7 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
       cta_bar();
       if (worker && total > 0) {  // pre-step: dots of element 0 against the prologue residual
         wait_next();
-        block_dots(slot_of(0), par, enb[0], zpart + (warp - 1) * 16);
+        block_dots(slot_of(0), par, enb[0], zpart + ww * 16);
       }
       cta_bar();
 
@@ -711,7 +716,7 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
           // workers: r -= W_{t-1} d_{t-1}, then (unless stopped) the dots of t+1
           if (t > 0) {
             const uint32_t e = t - 1;
-            const int li = (e & 1) * NWK + (warp - 1);
+            const int li = (e & 1) * NWK + ww;
             axpy_cols(slot_of(e), ldv + li * LCAP, lcp + li * LCAP, lcnt[li]);
           }
           PROF_LAP(0)
@@ -720,7 +725,7 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
             const uint32_t e = t + 1;
             wait_next();
             PROF_LAP(4)
-            block_dots(slot_of(e), par + 32 * (e & 3), enb[e & 3], zpart + ((e & 1) * NWK + warp - 1) * 16);
+            block_dots(slot_of(e), par + 32 * (e & 3), enb[e & 3], zpart + ((e & 1) * NWK + ww) * 16);
           }
           PROF_LAP(3)
           if (sweep_closed) {
@@ -730,10 +735,10 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
 #pragma unroll
             for (int k = 0; k < RPT; ++k) rr = fma(r[k], r[k], rr);
             rr = warp_sum(rr);
-            if (lane == 0) red[32 + 16 * (sw & 1) + warp - 1] = rr;
+            if (lane == 0) red[32 + 16 * (sw & 1) + ww] = rr;
           }
         }
-        else if (!stopped && t + 2 < total) {
+        else if (streamer && !stopped && t + 2 < total) {
           // stream warp: the parameter pipeline (global loads; nothing else waits on them)
           publish((t + 2) & 3);                             // packed at step t-1
           pack_raw();                                       // element t+3 (raw loads of step t-1)
@@ -771,7 +776,7 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
       if (blockIdx.x == 0 && tid == DT) printf("tma fit %d: %lld cycles for %lld bytes, %u issues\n", (int)s, tma_cyc, tma_bytes, q);
 #endif
 #ifdef PAM_BLK_PROF
-      if (blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == 1 || warp == NWK || warp == NWK + 1))
+      if (blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == 1 || warp == 5 || warp == 4))
         printf("blkprof fit %d warp %d nblk %d M %d: %lld %lld %lld %lld %lld %lld %lld %lld\n", (int)s, warp, nblk, M, pf_t[0], pf_t[1], pf_t[2], pf_t[3], pf_t[4], pf_t[5], pf_t[6], pf_t[7]);
 #endif
       if (max_iters == 0) {
@@ -797,7 +802,7 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
         cta_bar();
         if (tid == 32) {
           double rss = 0.0, t1 = 0.0, t2 = 0.0;
-          for (int w = 0; w < NWK + 2; ++w) {
+          for (int w = 0; w < NWARPS; ++w) {
             rss += red[w];
             t1 += red[20 + w];
             t2 += red[40 + w];
@@ -806,7 +811,7 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
         }
       }
       // observe every element issued beyond the stop (at most STAGES - 1 behind)
-      if (streamer) seen = q;  // never waited in the sweeps; phases are derived from ebase + seen
+      if (!solver && !worker) seen = q;  // stream / idle warps never waited in the sweeps; phases derive from ebase + seen
       while (seen < q) wait_next();
       cta_bar();
       if (tid == 32) {

@@ -1,8 +1,7 @@
 V=paper_2605_16564_b200/build/variants
-timeout 120 python tools/cd_probe.py C2 --rounds 1 --kernel block --iters 400 --lib $V/libpam_prof.so 2>&1 | grep -E "blkprof|cd_s" | tail -5
 for cfg in "C2 --rounds 1" "C2 --rounds 3" "C3 --rounds 2"; do
 for lib in old cur; do
   if [ $lib = cur ]; then L=""; else L="--lib $V/libpam_$lib.so"; fi
-  echo "== $cfg $lib"; timeout 300 python tools/cd_probe.py $cfg --kernel block --iters 400 --repeat 2 $L 2>&1 | tail -1
+  echo "== $cfg $lib"; timeout 60 python tools/cd_probe.py $cfg --kernel block --iters 400 --repeat 2 $L 2>&1 | tail -1
 done; done
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "kernel_choices or pipelined_few or 2d_refined or wide_gram" 2>&1 | tail -3
+timeout 400 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "kernel_choices or pipelined_few or 2d_refined or wide_gram" 2>&1 | tail -3
