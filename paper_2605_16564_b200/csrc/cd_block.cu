@@ -87,15 +87,14 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
   double* const slots = reinterpret_cast<double*>(smem_raw);
   double* const zpart = slots + STAGES * SLOT_D;  // [2][NWK][16] block dots per worker warp (element parity)
   double* const zraw = zpart + 2 * NWK * 16;      // [64] staging (beta0 of a prologue block)
-  double* const ldv = zraw + 64;                // [2][NWK][LCAP] nonzero block steps, per worker warp
-  double* const dfull = ldv + 2 * NWK * LCAP;   // [2][32] block steps by column (solver)
+  double* const dfull = zraw + 64;              // [2][32] block steps by column (element parity)
   double* const red = dfull + 64;               // [64] reductions (sweep-parity double-buffered)
   double* const sprm = red + 64;                // [20][4] solver: {beta, 1/denom, G[k][k-1], G[k][k-2]} of column k
   int* const par = reinterpret_cast<int*>(sprm + 80);  // [4][32] packed column parameters (element & 3)
   int* const enb = par + 128;                         // [4] columns of element (e & 3)
-  int* const lcp = enb + 4;                           // [2][NWK][LCAP] packed parameters of the listed columns
-  int* const lcnt = lcp + 2 * NWK * LCAP;             // [2][NWK] entries of each worker warp's list
-  int* const ctl = lcnt + 2 * NWK;  // [10]: nblk, next item, stop flags [2] (step parity), sweeps done, converged
+  int* const lcp = enb + 4;                           // [4][NWK][LCAP] per worker warp: the element's columns whose run meets its rows
+  int* const lcnt = lcp + 4 * NWK * LCAP;             // [4][NWK] entries of each list
+  int* const ctl = lcnt + 4 * NWK;  // [10]: nblk, next item, stop flags [2] (step parity), sweeps done, converged
   uint64_t* const bars = reinterpret_cast<uint64_t*>(ctl + 10);  // 8-byte aligned
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool solver = warp == 0;
@@ -261,15 +260,30 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
         pf_nb = rw_nb;
         pf_par = (lane < rw_nb) ? col_pack(static_cast<int>(rw_off) - rw_woff, tile_code(rw_mk)) : 0;
       };
+      // publish element buffer k: the packed parameters by column, and per worker warp w
+      // the list of the columns whose tile run meets w's rows (tiles RPT w .. RPT w +
+      // RPT - 1), in column order; a list entry is offset | column << 13 | a0 << 17 | la << 22
       auto publish = [&](int k) {
         par[32 * k + lane] = pf_par;
         if (lane == 0) enb[k] = pf_nb;
+        const int a0 = (pf_par >> 16) & 0xff, la = (pf_par >> 24) & 0xff;
+        const bool on = lane < pf_nb && la > 0;
+        const int wlo = a0 / RPT, whi = (a0 + la - 1) / RPT;
+        const int entry = (pf_par & 0x1fff) | (lane << 13) | (a0 << 17) | (la << 22);
+        const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+        for (int w = 0; w < NWK; ++w) {
+          const bool mine = on && wlo <= w && w <= whi;
+          const unsigned m = __ballot_sync(0xffffffffu, mine);
+          if (mine) lcp[(k * NWK + w) * LCAP + __popc(m & lt)] = entry;
+          if (lane == 0) lcnt[k * NWK + w] = __popc(m);
+        }
       };
-      // workers: rows -= sum_k dv[k] W_{column cpv[k]} over cnt columns of the block in
-      // slot Wb, four columns per pass (all four columns' loads are in flight before
-      // the FMAs; a column outside this thread's tile, or past cnt, contributes an
-      // exact zero step), in ascending k
-      auto axpy_cols = [&](const double* Wb, const double* dv, const int* cpv, int cnt) {
+      // workers: rows -= sum d_j W_j over the columns j of this warp's list (entries
+      // lst[0..cnt), steps dv[] by column), four columns per pass (all loads of a pass in
+      // flight before its FMAs; a tile outside the column's run, or an entry past cnt,
+      // contributes an exact zero), in column order
+      auto axpy_cols = [&](const double* Wb, const double* dv, const int* lst, int cnt) {
         const int tile0 = RPT * ww + (lane >> 4);  // tile of pair v: tile0 + 2 v
         const int sub = (2 * lane) & 31;
         const double2 zz = make_double2(0.0, 0.0);
@@ -279,16 +293,15 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const bool ok = k + u < cnt;
-            const int kk = ok ? k + u : k;
-            const int cp = cpv[kk];
-            const int o = cp & 0xffff, a0 = (cp >> 16) & 0xff, la = cp >> 24;
+            const int cp = lst[ok ? k + u : k];
+            const int o = cp & 0x1fff, j = (cp >> 13) & 15, a0 = (cp >> 17) & 31, la = cp >> 22;
 #pragma unroll
             for (int v = 0; v < RPT / 2; ++v) {
               const int tr = tile0 + 2 * v - a0;
               const bool in = ok && static_cast<unsigned>(tr) < static_cast<unsigned>(la);
               w[u][v] = in ? *reinterpret_cast<const double2*>(Wb + o + 32 * tr + sub) : zz;
             }
-            d[u] = dv[kk];
+            d[u] = dv[j];
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -321,32 +334,34 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
         }
         return warp_sum((s0 + s1) + (s2 + s3));
       };
-      // workers: the dots of a block of nb <= 16 columns against the residual, ROW
-      // parallel: each thread multiplies its own rows (registers) with the columns'
-      // entries of those rows, the warp adds its 32 lanes' 16 partial sums by a
-      // halving butterfly (16 -> 8 -> 4 -> 2 -> 1 values per lane, then the last
-      // lane pair) and lanes 0, 2, .., 30 store the warp's 16 column sums to zp[16];
-      // the solver adds the worker warps' parts in warp order.  No residual mirror
-      // in shared memory: per block the shared-memory traffic is the block's tiles,
-      // once for the dots and once for the AXPY.
-      auto block_dots = [&](const double* Wb, const int* pk, int nb, double* zp) {
+      // workers: the dots of a block's columns against the residual, ROW parallel: each
+      // thread multiplies its own rows (registers) with the entries of those rows in
+      // the columns of its warp's list (the columns whose run meets the warp's rows),
+      // the warp adds its 32 lanes' partial sums by a halving butterfly (16 -> 8 ->
+      // 4 -> 2 -> 1 values per lane, or 8 -> .. for lists of <= 8 columns) and the
+      // lanes holding a total store it to the column's entry of zp[16] (zero for the
+      // columns not on the list); the solver adds the worker warps' parts in warp
+      // order.  No residual mirror in shared memory: per block the shared-memory
+      // traffic is the block's tiles, once for the dots and once for the AXPY.
+      auto block_dots = [&](const double* Wb, const int* lst, int cnt, double* zp) {
         const int tile0 = RPT * ww + (lane >> 4);  // tile of pair v: tile0 + 2 v
         const int sub = (2 * lane) & 31;
         const double2 zz = make_double2(0.0, 0.0);
         double p[16];
+        if (lane < 16) zp[lane] = 0.0;
 #pragma unroll
         for (int j0 = 0; j0 < 16; j0 += 4) {
-          if (j0 < nb) {
+          if (j0 < cnt) {
             double2 w[4][RPT / 2];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const int j = j0 + u;
-              const int cp = pk[j < nb ? j : j0];
-              const int o = cp & 0xffff, a0 = (cp >> 16) & 0xff, la = cp >> 24;
+              const bool ok = j0 + u < cnt;
+              const int cp = lst[ok ? j0 + u : j0];
+              const int o = cp & 0x1fff, a0 = (cp >> 17) & 31, la = cp >> 22;
 #pragma unroll
               for (int v = 0; v < RPT / 2; ++v) {
                 const int tr = tile0 + 2 * v - a0;
-                const bool in = j < nb && static_cast<unsigned>(tr) < static_cast<unsigned>(la);
+                const bool in = ok && static_cast<unsigned>(tr) < static_cast<unsigned>(la);
                 w[u][v] = in ? *reinterpret_cast<const double2*>(Wb + o + 32 * tr + sub) : zz;
               }
             }
@@ -365,23 +380,43 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
             for (int u = 0; u < 4; ++u) p[j0 + u] = 0.0;
           }
         }
-        // halving butterfly: after the level with lane bit b, a lane keeps the half
-        // of its values selected by that bit
+        __syncwarp();  // the zeroed zp is ordered before the totals below
+        int pos;       // list position of the total this lane ends up holding
+        double tot;
+        if (cnt > 8) {
 #pragma unroll
-        for (int lvl = 0; lvl < 4; ++lvl) {
-          const int half = 8 >> lvl;           // values kept after this level
-          const int bit = 16 >> lvl;           // lane bit of this level
-          const bool hi = (lane & bit) != 0;
+          for (int lvl = 0; lvl < 4; ++lvl) {
+            const int half = 8 >> lvl;  // values kept after this level
+            const int bit = 16 >> lvl;  // lane bit of this level
+            const bool hi = (lane & bit) != 0;
 #pragma unroll
-          for (int i = 0; i < half; ++i) {
-            const double keep = hi ? p[i + half] : p[i];
-            const double send = hi ? p[i] : p[i + half];
-            p[i] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
+            for (int i = 0; i < half; ++i) {
+              const double keep = hi ? p[i + half] : p[i];
+              const double send = hi ? p[i] : p[i + half];
+              p[i] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
+            }
           }
+          tot = p[0] + __shfl_xor_sync(0xffffffffu, p[0], 1);
+          pos = lane >> 1;
+        } else {
+#pragma unroll
+          for (int lvl = 0; lvl < 3; ++lvl) {
+            const int half = 4 >> lvl;
+            const int bit = 16 >> lvl;
+            const bool hi = (lane & bit) != 0;
+#pragma unroll
+            for (int i = 0; i < half; ++i) {
+              const double keep = hi ? p[i + half] : p[i];
+              const double send = hi ? p[i] : p[i + half];
+              p[i] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
+            }
+          }
+          double t2 = p[0] + __shfl_xor_sync(0xffffffffu, p[0], 2);
+          tot = t2 + __shfl_xor_sync(0xffffffffu, t2, 1);
+          pos = lane >> 2;
         }
-        const double tot = p[0] + __shfl_xor_sync(0xffffffffu, p[0], 1);
-        // value index held by this lane: bit 4 of the lane -> bit 3 of the index, ...
-        if ((lane & 1) == 0) zp[lane >> 1] = tot;
+        const bool holder = (cnt > 8) ? (lane & 1) == 0 : (lane & 3) == 0;
+        if (holder && pos < cnt) zp[(lst[pos] >> 13) & 15] = tot;
       };
       // ---- prologue pass: col_sq (elastic_net.py:85), r = y - W beta0 (94), and the
       //      diagonal and previous-block Gram blocks; elements 0..nblk-1, then block 0
@@ -438,7 +473,10 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
             }
             Gf[(diag ? bk.gd : bk.go) + k * nb + c] = g;
           }
-          if (!wrap && worker) axpy_cols(Wb, zraw, pk, nb);  // r -= W_b beta0_b
+          if (!wrap && worker) {  // r -= W_b beta0_b
+            const int li = static_cast<int>(e & 3) * NWK + ww;
+            axpy_cols(Wb, zraw, lcp + li * LCAP, lcnt[li]);
+          }
           asm volatile("fence.proxy.async.global;" ::: "memory");  // the sweeps re-read G by TMA
           cta_bar();  // slot e-1 free
           if (q < np_el) {
@@ -482,14 +520,13 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
           pd = blk[modn(4)];        // columns loaded at step 0
         }
       }
-      if (tid < 2 * NWK) lcnt[tid] = 0;
       if (tid < 64) dfull[tid] = 0.0;
       if (tid < 2) ctl[2 + tid] = 0;  // stop flags (step parity)
       if (tid == 0) ctl[4] = ctl[5] = 0;  // sweeps done, converged
       cta_bar();
       if (worker && total > 0) {  // pre-step: dots of element 0 against the prologue residual
         wait_next();
-        block_dots(slot_of(0), par, enb[0], zpart + ww * 16);
+        block_dots(slot_of(0), lcp + ww * LCAP, lcnt[ww], zpart + ww * 16);
       }
       cta_bar();
 
@@ -659,28 +696,9 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
               }
             }
             PROF_LAP(3)
-            // steps by column (solver's correction next step), and per worker warp the
-            // list of the nonzero steps whose column run meets that warp's rows (tiles
-            // RPT w .. RPT w + RPT - 1), in column order (d == 0 leaves r unchanged)
-            {
-              const int a0 = (pkc >> 16) & 0xff, la = (pkc >> 24) & 0xff;
-              const bool nz = lane < nb && dc != 0.0 && la > 0;
-              const int wlo = a0 / RPT, whi = (a0 + la - 1) / RPT;
-              const unsigned lt = (1u << lane) - 1u;
-              int* const lc = lcp + (t & 1) * NWK * LCAP;
-              double* const lv = ldv + (t & 1) * NWK * LCAP;
-#pragma unroll
-              for (int w = 0; w < NWK; ++w) {
-                const bool mine = nz && wlo <= w && w <= whi;
-                const unsigned m = __ballot_sync(0xffffffffu, mine);
-                if (mine) {
-                  const int pos = __popc(m & lt);
-                  lc[w * LCAP + pos] = pkc;
-                  lv[w * LCAP + pos] = dc;
-                }
-                if (lane == 0) lcnt[(t & 1) * NWK + w] = __popc(m);
-              }
-            }
+            // steps by column for the workers' AXPY (their per-warp column lists were built
+            // by the stream warp when it published the block)
+            dfull[32 * (t & 1) + lane] = (lane < nb) ? dc : 0.0;
             // the block's coefficients go to global memory at the top of the NEXT step:
             // a store issued right before the CTA barrier holds every warp at the barrier
             // until it is performed (~700 cycles per step, 40 % of all stall samples)
@@ -716,8 +734,8 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
           // workers: r -= W_{t-1} d_{t-1}, then (unless stopped) the dots of t+1
           if (t > 0) {
             const uint32_t e = t - 1;
-            const int li = (e & 1) * NWK + ww;
-            axpy_cols(slot_of(e), ldv + li * LCAP, lcp + li * LCAP, lcnt[li]);
+            const int li = static_cast<int>(e & 3) * NWK + ww;
+            axpy_cols(slot_of(e), dfull + 32 * (e & 1), lcp + li * LCAP, lcnt[li]);
           }
           PROF_LAP(0)
           PROF_LAP(1)
@@ -725,7 +743,8 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
             const uint32_t e = t + 1;
             wait_next();
             PROF_LAP(4)
-            block_dots(slot_of(e), par + 32 * (e & 3), enb[e & 3], zpart + ((e & 1) * NWK + ww) * 16);
+            const int li = static_cast<int>(e & 3) * NWK + ww;
+            block_dots(slot_of(e), lcp + li * LCAP, lcnt[li], zpart + ((e & 1) * NWK + ww) * 16);
           }
           PROF_LAP(3)
           if (sweep_closed) {
@@ -837,8 +856,8 @@ int64_t cd_block_workspace_bytes(int64_t S, int64_t total_slots) {
 template <int SLOT_WD, int GMAX, int MINB>
 int launch_block_pipe_cfg(const CdArgs& a, void* block_ws, cudaStream_t stream) {
   using namespace bp;
-  const size_t smem = static_cast<size_t>(STAGES) * (SLOT_WD + 2 * GMAX * GMAX) * 8 + (2 * NWK * 16 + 64 * 3 + 80 + 2 * NWK * LCAP) * 8 +
-                      (128 + 4 + 2 * NWK * LCAP + 2 * NWK + 10) * 4 + 8 * STAGES + 16;
+  const size_t smem = static_cast<size_t>(STAGES) * (SLOT_WD + 2 * GMAX * GMAX) * 8 + (2 * NWK * 16 + 64 * 3 + 80) * 8 +
+                      (128 + 4 + 4 * NWK * LCAP + 4 * NWK + 10) * 4 + 8 * STAGES + 16;
   auto kernel = cd_block_kernel<SLOT_WD, GMAX, MINB>;
   PAM_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   PAM_CUDA_CHECK(cudaMemsetAsync(a.queue, 0, sizeof(unsigned), stream));
