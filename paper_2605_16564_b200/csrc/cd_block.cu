@@ -9,31 +9,42 @@
 // (dot -> warp reduction -> soft threshold -> AXPY, ~0.55 us per column,
 // profiles/r01_ncu_cd_pair_c2_raw.csv: FP64 pipe 4 %, DRAM 0.05 of peak) IS
 // the runtime.  Columns are therefore taken in blocks (<= 16 columns whose
-// packed tiles fit a shared-memory slot): all dots of a block at once
-// (column-parallel, one warp per column), the block's cyclic updates in order
-// through its diagonal Gram block G_bb (one solver warp, one shuffle + the soft
-// threshold + one FMA per column on the serial path), one row-parallel AXPY
-// for the block.  The first, unpipelined version of this (round 2) ran the
-// three phases back to back and left 8 of 9 warps idle during the solve
-// (37 % of stall samples, profiles/r02_ncu_cd_block_c2_lines.txt); here block
-// t's solve overlaps block t-1's AXPY and block t+1's dots:
+// packed tiles fit a shared-memory slot) and a CTA per fit works on three blocks
+// at once:
 //
-//   workers (8 warps), step t:  r -= W_{t-1} d_{t-1};  zraw_{t+1} = W_{t+1}^T r
-//   solver  (1 warp),  step t:  z_t = zraw_t - G[t, t-1] d_{t-1};  in-block
+//   workers (8 warps), step t:  r -= W_{t-1} d_{t-1};  zpart_{t+1} = W_{t+1}^T r
+//   solver  (1 warp),  step t:  z_t = sum zpart_t - G[t, t-1] d_{t-1};  in-block
 //                               cyclic updates of block t -> d_t
+//   stream  (1 warp),  step t:  block t+2's column parameters and per-worker column
+//                               lists; the bulk copy of block t+3 after the barrier
 //
-// zraw_{t+1} is formed against the residual BEFORE block t's updates; the
+// zpart_{t+1} is formed against the residual BEFORE block t's updates; the
 // missing term is exactly -G[t+1, t] d_t (G = W^T W restricted to the two
-// blocks), applied by the solver at the start of step t+1 -- the same
+// blocks), accumulated by the solver inside step t's update loop -- the same
 // identity as the in-block corrections, now across the block boundary, so the
 // update sequence is still the reference's cyclic order j = 0..M-1, sweep
 // after sweep (elastic_net.py:137-161); only the rounding of the inner
-// products differs (~1e-12, the SURVEY F2 class).  The stream of blocks is
-// continuous across sweeps (block 0 of sweep k+1 follows block nblk-1 of sweep
-// k, with G[0, nblk-1]).  The diagonal and the off-diagonal (previous-block)
-// Gram blocks are computed once per round in the prologue pass and streamed
-// with the block.  One end-of-step CTA barrier per block; the workers add one
-// named barrier between their AXPY and their dots.
+// products (and of the quotient, see the solver loop) differs, ~1e-12, the
+// SURVEY F2 class.  The stream of blocks is continuous across sweeps (block 0
+// of sweep k+1 follows block nblk-1 of sweep k, with G[0, nblk-1]).  The
+// diagonal and the previous-block Gram blocks are computed once per round in
+// the prologue pass and streamed with the block.  One CTA barrier per step.
+//
+// Round-2 session-4 structure (profiles/r02_cd_block_ab_s4.txt: C2 4.08 -> 3.0 s,
+// C3 12.4 -> 8.8 s, Table-2 6.0 -> 4.35 s):
+//  * workers are ROW parallel in both phases: a thread keeps its 4 residual rows
+//    in registers, so the dots need no residual mirror in shared memory (the
+//    block's tiles are the only shared-memory traffic, read once for the dots
+//    and once for the AXPY; the column-parallel dots re-read the residual and
+//    were shared-memory-bandwidth bound) and no barrier between AXPY and dots;
+//    a warp's 16 partial sums go through a halving butterfly;
+//  * the stream warp builds, per worker warp, the list of the block's columns
+//    whose tile run meets that warp's rows: dots and AXPY visit only those;
+//  * the solver's serial chain per column is one FMA, the shift by lam1, one
+//    multiply by 1 / (col_sq + lam2) and the sign selects (the next column's value
+//    is broadcast two steps early and corrected through G[k][k-1], G[k][k-2]);
+//  * the solver warp has issue scheduler 0 to itself (warp placement below);
+//  * block / sweep indices are carried incrementally (no division by nblk).
 #include "cd_common.cuh"
 
 #include <algorithm>
@@ -62,12 +73,12 @@ constexpr int NWK = PAM_BLK_NWK;    // worker warps
 // 0 to itself -- its ~60-instruction serial stream per column gets every issue
 // slot -- sharing it only with the stream warp (4, a few instructions per step) and
 // an idle warp (8); the worker warps are the ones with w % 4 != 0.
-constexpr int NWARPS = NWK + 1 + (NWK + 2) / 3;  // NWK = 8: warps 0..10
+constexpr int NWARPS = NWK + (NWK - 1) / 3 + 1;  // NWK = 8: warps 0..10
 constexpr int NT = NWARPS * 32;
 constexpr int DT = 4 * 32;  // the stream warp's issuing thread
 constexpr int RPT = 1024 / (NWK * 32);  // residual rows per worker thread (= tiles per worker warp)
 static_assert(RPT == 2 || RPT == 4, "worker row ownership: two or four consecutive rows per thread");
-constexpr int LCAP = 16;            // entries per worker warp's AXPY list (= GMAX)
+constexpr int LCAP = 16;            // entries per worker warp's column list (= GMAX)
 constexpr int64_t WS_PER_SLOT = 576;  // 32 B descriptor + 2 x 33 Gram doubles (+ padding) per slot
 constexpr int64_t WS_PER_FIT = 96;
 
