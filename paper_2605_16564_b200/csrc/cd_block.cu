@@ -77,7 +77,7 @@ constexpr int NWARPS = NWK + (NWK - 1) / 3 + 1;  // NWK = 8: warps 0..10
 constexpr int NT = NWARPS * 32;
 constexpr int DT = 4 * 32;  // the stream warp's issuing thread
 constexpr int RPT = 1024 / (NWK * 32);  // residual rows per worker thread (= tiles per worker warp)
-static_assert(RPT == 2 || RPT == 4, "worker row ownership: two or four consecutive rows per thread");
+static_assert(RPT == 4 && NWK == 8, "worker row ownership and the fixed 8-warp sums assume 8 worker warps of 4 rows per thread");
 constexpr int LCAP = 16;            // entries per worker warp's column list (= GMAX)
 constexpr int64_t WS_PER_SLOT = 576;  // 32 B descriptor + 2 x 33 Gram doubles (+ padding) per slot
 constexpr int64_t WS_PER_FIT = 96;
@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
       unsigned char* const wsf = ws + doff * WS_PER_SLOT + s * WS_PER_FIT;
       Blk* blk = reinterpret_cast<Blk*>(wsf);
       double* Gf = reinterpret_cast<double*>(wsf + sizeof(Blk) * (M + 1));
+      double* invs = Gf + 32 * static_cast<int64_t>(M);  // 1 / (col_sq + lam2) by column (Gram blocks take <= 32 doubles per column)
       const double lam1 = a.lam1[s], lam2 = a.lam2[s], tol = a.tol[s];
       const int max_iters = a.max_iters[s];
 
@@ -455,7 +456,11 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
           if (!wrap) {
             for (int j = warp; j < nb; j += NWARPS) {
               const double cs = col_sq_dot(Wb, pk[j]);
-              if (lane == 0) colsq[bk.j0 + j] = cs;
+              if (lane == 0) {
+                colsq[bk.j0 + j] = cs;
+                const double dn = __dadd_rn(cs, lam2);
+                invs[bk.j0 + j] = dn > 0.0 ? __ddiv_rn(1.0, dn) : 0.0;
+              }
             }
           }
           // Gram blocks: diagonal G[c][k] (not for the wrap element) and previous-block
@@ -544,11 +549,12 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
       // solver state: lane c <-> column c of the current block; descriptors and the
       // next block's beta / col_sq are register-pipelined (no global load on the chain)
       double bc = 0.0, csc = 0.0;
-      double nbx = 0.0, ncs = 0.0;  // beta / col_sq of element t+1
+      double nbx = 0.0, ncs = 0.0, ninv = 0.0;  // beta / col_sq / 1 / (col_sq + lam2) of element t+1
       Blk sd_cur, sd_n1, sd_n2;     // descriptors of elements t, t+1, t+2
       auto sprefetch = [&](const Blk& bk) {
         nbx = (lane < bk.nb) ? betas[bk.j0 + lane] : 0.0;
         ncs = (lane < bk.nb) ? colsq[bk.j0 + lane] : 0.0;
+        ninv = (lane < bk.nb) ? invs[bk.j0 + lane] : 0.0;  // 1 / (col_sq + lam2), from the prologue
       };
       if (solver && total > 0) {
         sd_n1 = blk[0];
@@ -557,7 +563,7 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
       }
       double max_delta = 0.0, acc_l1 = 0.0, acc_l2 = 0.0, acc_max = 0.0;  // solver, per sweep
       double corr = 0.0;  // solver: G[t, t-1] d_{t-1} of this lane's column (accumulated during step t-1)
-      double invc = 0.0, ninv = 0.0;    // 1 / (col_sq + lam2) of this / the next block's column
+      double invc = 0.0;                // 1 / (col_sq + lam2) of this block's column
       double g1n = 0.0, g2n = 0.0;      // next block's G[c][c-1], G[c][c-2] (read from its slot a step early)
       int pkn = 0;                      // next block's packed column parameters
       bool first_blk = true;
@@ -580,10 +586,6 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
             if (nblk > 1 || t == 0) {
               bc = nbx;
               csc = ncs;
-              if (t == 0) {
-                const double dn0 = __dadd_rn(ncs, lam2);
-                ninv = dn0 > 0.0 ? __ddiv_rn(1.0, dn0) : 0.0;
-              }
               invc = ninv;
             }
             if (nblk > 1 && t + 1 < total) sprefetch(sd_n1);  // its betas were written by this lane
@@ -607,8 +609,7 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
               double zw[NWK];
 #pragma unroll
               for (int w = 0; w < NWK; ++w) zw[w] = zb[16 * w];
-#pragma unroll
-              for (int w = 0; w < NWK; ++w) zsum += zw[w];  // worker warps in order
+              zsum = ((zw[0] + zw[1]) + (zw[2] + zw[3])) + ((zw[4] + zw[5]) + (zw[6] + zw[7]));  // fixed tree over the worker warps
             }
             const double zdot = (lane < nb) ? __dsub_rn(zsum, corr) : 0.0;
             double zc = __dadd_rn(__dmul_rn(csc, bc), zdot);
@@ -693,18 +694,13 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
             }
             corr = cr0 + cr1;
             // next block: its sub-diagonal Gram entries and column parameters (slot t+1 is
-            // resident, parameters published two steps ago) and 1 / (col_sq + lam2) of the
-            // col_sq prefetched at the top of this step -- all off the next step's chain
+            // resident, parameters published two steps ago) -- off the next step's chain
             if (has_next) {
               const double* Gd1 = slot_of(t + 1) + SLOT_WD;
               const bool on1 = lane < nb1;
               g1n = (on1 && lane > 0) ? Gd1[(lane - 1) * nb1 + lane] : 0.0;
               g2n = (on1 && lane > 1) ? Gd1[(lane - 2) * nb1 + lane] : 0.0;
               pkn = par[32 * ((t + 1) & 3) + lane];
-              if (nblk > 1) {
-                const double dn1 = __dadd_rn(ncs, lam2);
-                ninv = dn1 > 0.0 ? __ddiv_rn(1.0, dn1) : 0.0;
-              }
             }
             PROF_LAP(3)
             // steps by column for the workers' AXPY (their per-warp column lists were built
