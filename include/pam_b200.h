@@ -59,9 +59,10 @@ extern "C" {
 #define PAM_ERR_NONPOSITIVE 5  /* field value not positive (elastic_net.py:200-204) */
 #define PAM_ERR_UNSUPPORTED 6  /* shape outside the compiled kernel envelope       */
 #define PAM_ERR_NONFINITE 7    /* non-finite design/target (elastic_net.py:81-82)  */
+#define PAM_ERR_CLAIMED 8      /* point claimed by two boxes (geometry.py:249-251)  */
 
 /* Version / capability probe: returns PAM_ABI_VERSION. */
-#define PAM_ABI_VERSION 2
+#define PAM_ABI_VERSION 3
 int pam_abi_version(void);
 /* Last CUDA error string recorded by the library (host memory, static). */
 const char* pam_last_error(void);
@@ -304,6 +305,26 @@ int pam_eval_f64(int dim, int64_t P, const double* pts, const int32_t* shape,
                  const int32_t* m_cur, const double* centres, const double* widths,
                  const double* beta, const int32_t* log_flag, double* out,
                  void* work, int64_t* err, void* stream);
+
+/* The same for ARBITRARY half-open boxes (geometry.py:54-66, 242-258, the
+ * reference's locate_many accepts any box set): box i = [lo, hi) per axis, the
+ * upper face closed where box_open[i*dim + k] == 0; owner = the first box, in
+ * order, containing the point.  Errors as the reference raises them: a point
+ * inside two boxes -> err {CLAIMED, second box << 40 | point} (the first box,
+ * in order, that re-claims a point; checked before coverage), a point in no
+ * box -> err {OUTSIDE, j}.  S < 2^23, P < 2^40.  pam_locate_boxes_f64 needs
+ * 16 bytes of scratch in `work`; pam_eval_boxes_f64 the scratch of
+ * pam_eval_workspace_bytes(P, S). */
+int pam_locate_boxes_f64(int dim, int64_t P, const double* pts, int64_t S,
+                         const double* box_lo, const double* box_hi,
+                         const int32_t* box_open, int64_t* owner, void* work,
+                         int64_t* err, void* stream);
+int pam_eval_boxes_f64(int dim, int64_t P, const double* pts, const double* box_lo,
+                       const double* box_hi, const int32_t* box_open, int64_t S,
+                       const int64_t* dict_off, const int32_t* m_cur,
+                       const double* centres, const double* widths, const double* beta,
+                       const int32_t* log_flag, double* out, void* work, int64_t* err,
+                       void* stream);
 
 /* Shepard evaluation of ONE dictionary at P points (rbf.py:152-167):
  * out[j] = (sum_m e_jm beta_m) / (sum_m e_jm), e = exp(L - rowmax). */

@@ -21,7 +21,7 @@ from .errors import NumericalError
 
 LIB_PATH = Path(__file__).resolve().parent / "libpam_b200.so"
 
-ABI_VERSION = 2  # PAM_ABI_VERSION of include/pam_b200.h
+ABI_VERSION = 3  # PAM_ABI_VERSION of include/pam_b200.h
 
 # status codes (pam_b200.h)
 PAM_OK = 0
@@ -32,6 +32,7 @@ PAM_ERR_DEGENERATE = 4
 PAM_ERR_NONPOSITIVE = 5
 PAM_ERR_UNSUPPORTED = 6
 PAM_ERR_NONFINITE = 7
+PAM_ERR_CLAIMED = 8
 
 _i32 = ctypes.c_int32
 _i64 = ctypes.c_int64
@@ -93,6 +94,12 @@ SIGNATURES = {
     ),
     "pam_eval_workspace_bytes": (_i64, [_i64, _i64]),
     "pam_locate_f64": (ctypes.c_int, [ctypes.c_int, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr]),
+    "pam_locate_boxes_f64": (ctypes.c_int, [ctypes.c_int, _i64, _ptr, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr]),
+    "pam_eval_boxes_f64": (
+        ctypes.c_int,
+        [ctypes.c_int, _i64, _ptr, _ptr, _ptr, _ptr, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr,
+         _ptr, _ptr],
+    ),
     "pam_eval_f64": (
         ctypes.c_int,
         [ctypes.c_int, _i64, _ptr, _ptr, _ptr, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr,
@@ -173,7 +180,7 @@ class _CountingLib:
     KERNELS_PER_CALL = {
         "pam_err_reset": 1, "pam_log_values_f64": 1, "pam_assemble_f64": 1, "pam_cd_f64": 1,
         "pam_cd_ex_f64": 1, "pam_residual_f64": 2, "pam_mark_f64": 1, "pam_enrich_f64": 1,
-        "pam_locate_f64": 1, "pam_eval_f64": 5, "pam_shepard_eval_f64": 1,
+        "pam_locate_f64": 1, "pam_locate_boxes_f64": 2, "pam_eval_f64": 5, "pam_eval_boxes_f64": 6, "pam_shepard_eval_f64": 1,
         "pam_row_normalize_f64": 1, "pam_gather_cells_f64": 1, "pam_dict_scatter_f64": 1, "pam_assemble_tiles_f64": 3,
         "pam_cd_tiles_f64": 1, "pam_gram_f64": 2, "pam_cd_gram_f64": 1, "pam_probe_fp64": 1,
         "pam_p1_values_f64": 1, "pam_csr_spmv_f64": 1, "pam_pcg_f64": 3, "pam_c5_generate_f64": 2,  # + 5 per PCG iteration

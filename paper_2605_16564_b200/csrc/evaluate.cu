@@ -61,6 +61,50 @@ __global__ void locate_kernel(int64_t P, const double* __restrict__ pts,
   }
 }
 
+// Arbitrary half-open boxes (geometry.py:54-66, 242-258): per point the boxes are
+// tested in order; owner = the first box containing it.  A second containing box
+// records min over points of (second box << 40 | point) in flags[0] (the
+// reference raises for the FIRST box, in order, that re-claims a point, and within
+// it the smallest point index); a point in no box records its index in flags[1].
+template <int D, typename IdxT>
+__global__ void locate_boxes_kernel(int64_t P, const double* __restrict__ pts, int64_t S,
+                                    const double* __restrict__ lo, const double* __restrict__ hi,
+                                    const int32_t* __restrict__ open_hi, IdxT* __restrict__ owner,
+                                    unsigned long long* flags) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < P;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    double x[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) x[k] = pts[j * D + k];
+    int64_t own = -1;
+    for (int64_t i = 0; i < S; ++i) {
+      bool in = true;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const double l = lo[i * D + k], h = hi[i * D + k];
+        in = in && (x[k] >= l) && (open_hi[i * D + k] ? (x[k] < h) : (x[k] <= h));
+      }
+      if (in) {
+        if (own < 0) {
+          own = i;
+        } else {
+          atomicMin(flags, (static_cast<unsigned long long>(i) << 40) | static_cast<unsigned long long>(j));
+          break;
+        }
+      }
+    }
+    if (own < 0) atomicMin(flags + 1, static_cast<unsigned long long>(j));
+    owner[j] = static_cast<IdxT>(own);
+  }
+}
+
+// error word from the two flags: a doubly claimed point wins over an unclaimed one
+// (the reference checks claims inside its box loop, coverage after it)
+__global__ void locate_boxes_finish_kernel(const unsigned long long* flags, int64_t* err) {
+  if (flags[0] != ~0ull) report_error(err, PAM_ERR_CLAIMED, static_cast<int64_t>(flags[0]));
+  else if (flags[1] != ~0ull) report_error(err, PAM_ERR_OUTSIDE, static_cast<int64_t>(flags[1]));
+}
+
 // unsigned counterpart for atomicAdd (int32 -> unsigned, int64 -> unsigned long long)
 template <typename IdxT>
 using UIdx = std::conditional_t<sizeof(IdxT) == 8, unsigned long long, unsigned int>;
@@ -424,7 +468,24 @@ namespace pam {
 // locate -> counting sort by owner -> evaluation, with IdxT-wide indices
 // (int32 whenever P and S fit: half the sort traffic and 32-bit atomics)
 template <typename IdxT>
+int locate_boxes(int dim, int64_t P, const double* pts, int64_t S, const double* lo, const double* hi,
+                 const int32_t* open_hi, IdxT* owner, unsigned long long* flags, int64_t* err,
+                 cudaStream_t st) {
+  PAM_CUDA_CHECK(cudaMemsetAsync(flags, 0xff, 2 * sizeof(unsigned long long), st));
+  const int g = grid_for(P, 256);
+  if (dim == 1) locate_boxes_kernel<1, IdxT><<<g, 256, 0, st>>>(P, pts, S, lo, hi, open_hi, owner, flags);
+  else if (dim == 2) locate_boxes_kernel<2, IdxT><<<g, 256, 0, st>>>(P, pts, S, lo, hi, open_hi, owner, flags);
+  else locate_boxes_kernel<3, IdxT><<<g, 256, 0, st>>>(P, pts, S, lo, hi, open_hi, owner, flags);
+  PAM_LAUNCH_CHECK("locate_boxes_kernel");
+  locate_boxes_finish_kernel<<<1, 1, 0, st>>>(flags, err);
+  PAM_LAUNCH_CHECK("locate_boxes_finish_kernel");
+  return PAM_OK;
+}
+
+// shape/edges != null: tensor-grid boxes; else the S boxes (lo, hi, open_hi)
+template <typename IdxT>
 int eval_pipeline(int dim, int64_t P, const double* pts, const int32_t* shape, const double* edges,
+                  const double* box_lo, const double* box_hi, const int32_t* box_open,
                   int64_t S, const int64_t* dict_off, const int32_t* m_cur, const double* centres,
                   const double* widths, const double* beta, const int32_t* log_flag, double* out,
                   void* work, int64_t* err, cudaStream_t st) {
@@ -439,10 +500,15 @@ int eval_pipeline(int dim, int64_t P, const double* pts, const int32_t* shape, c
   unsigned long long* queue = reinterpret_cast<unsigned long long*>(
       (reinterpret_cast<uintptr_t>(start + S + 1) + 7) & ~static_cast<uintptr_t>(7));
   const int g = grid_for(P, 256);
-  if (dim == 1) locate_kernel<1, IdxT><<<g, 256, 0, st>>>(P, pts, shape, edges, owner, err);
-  else if (dim == 2) locate_kernel<2, IdxT><<<g, 256, 0, st>>>(P, pts, shape, edges, owner, err);
-  else locate_kernel<3, IdxT><<<g, 256, 0, st>>>(P, pts, shape, edges, owner, err);
-  PAM_LAUNCH_CHECK("locate_kernel");
+  if (shape != nullptr) {
+    if (dim == 1) locate_kernel<1, IdxT><<<g, 256, 0, st>>>(P, pts, shape, edges, owner, err);
+    else if (dim == 2) locate_kernel<2, IdxT><<<g, 256, 0, st>>>(P, pts, shape, edges, owner, err);
+    else locate_kernel<3, IdxT><<<g, 256, 0, st>>>(P, pts, shape, edges, owner, err);
+    PAM_LAUNCH_CHECK("locate_kernel");
+  } else {
+    const int rc = locate_boxes<IdxT>(dim, P, pts, S, box_lo, box_hi, box_open, owner, queue + 1, err, st);
+    if (rc != PAM_OK) return rc;
+  }
   PAM_CUDA_CHECK(cudaMemsetAsync(counts, 0, S * sizeof(IdxT), st));
   histogram_kernel<IdxT><<<g, 256, 0, st>>>(P, owner, counts);
   PAM_LAUNCH_CHECK("histogram_kernel");
@@ -473,10 +539,35 @@ extern "C" int pam_eval_f64(int dim, int64_t P, const double* pts, const int32_t
   if (P == 0) return PAM_OK;
   cudaStream_t st = as_stream(stream);
   if (P < 0x7fffffffLL && S < 0x7fffffffLL)
-    return eval_pipeline<int32_t>(dim, P, pts, shape, edges, S, dict_off, m_cur, centres, widths, beta,
-                                  log_flag, out, work, err, st);
-  return eval_pipeline<int64_t>(dim, P, pts, shape, edges, S, dict_off, m_cur, centres, widths, beta,
-                                log_flag, out, work, err, st);
+    return eval_pipeline<int32_t>(dim, P, pts, shape, edges, nullptr, nullptr, nullptr, S, dict_off, m_cur,
+                                  centres, widths, beta, log_flag, out, work, err, st);
+  return eval_pipeline<int64_t>(dim, P, pts, shape, edges, nullptr, nullptr, nullptr, S, dict_off, m_cur,
+                                centres, widths, beta, log_flag, out, work, err, st);
+}
+
+extern "C" int pam_locate_boxes_f64(int dim, int64_t P, const double* pts, int64_t S, const double* box_lo,
+                                    const double* box_hi, const int32_t* box_open, int64_t* owner,
+                                    void* work, int64_t* err, void* stream) {
+  if (dim < 1 || dim > 3 || P < 0 || S < 1 || S >= (1LL << 23) || P >= (1LL << 40) || !work) return PAM_ERR_ARG;
+  if (P == 0) return PAM_OK;
+  return locate_boxes<int64_t>(dim, P, pts, S, box_lo, box_hi, box_open, owner,
+                               static_cast<unsigned long long*>(work), err, as_stream(stream));
+}
+
+extern "C" int pam_eval_boxes_f64(int dim, int64_t P, const double* pts, const double* box_lo,
+                                  const double* box_hi, const int32_t* box_open, int64_t S,
+                                  const int64_t* dict_off, const int32_t* m_cur, const double* centres,
+                                  const double* widths, const double* beta, const int32_t* log_flag,
+                                  double* out, void* work, int64_t* err, void* stream) {
+  if (dim < 1 || dim > 3 || P < 0 || S < 1 || S >= (1LL << 23) || P >= (1LL << 40) || !work) return PAM_ERR_ARG;
+  if (!box_lo || !box_hi || !box_open) return PAM_ERR_ARG;
+  if (P == 0) return PAM_OK;
+  cudaStream_t st = as_stream(stream);
+  if (P < 0x7fffffffLL)
+    return eval_pipeline<int32_t>(dim, P, pts, nullptr, nullptr, box_lo, box_hi, box_open, S, dict_off, m_cur,
+                                  centres, widths, beta, log_flag, out, work, err, st);
+  return eval_pipeline<int64_t>(dim, P, pts, nullptr, nullptr, box_lo, box_hi, box_open, S, dict_off, m_cur,
+                                centres, widths, beta, log_flag, out, work, err, st);
 }
 
 extern "C" int pam_shepard_eval_f64(int dim, int64_t P, const double* pts, int64_t M,

@@ -187,19 +187,21 @@ class GlobalSurrogate:
         object.__setattr__(self, "_device_cache", ds)
 
     def _grid_dev(self):
+        """Device copy of the box geometry: ("grid", dim, shape, edges) for tensor-grid
+        partitions, ("boxes", dim, lo, hi, open_hi) for any other box set."""
         from . import _native as nat
+        from .geometry import box_arrays
 
         g = self.__dict__.get("_grid_cache")
         if g is None:
             grid = self.partition.grid
             if grid is None:
-                raise ValueError(
-                    "partition boxes do not form a half-open tensor grid; GlobalSurrogate.evaluate "
-                    "requires a make_partition-style decomposition"
-                )
-            shape, edges = grid
-            g = (len(shape), nat.to_dev(np.asarray(shape, dtype=np.int32)),
-                 nat.to_dev(np.concatenate(edges)))
+                lo, hi, op = box_arrays(self.partition.boxes)
+                g = ("boxes", lo.shape[1], nat.to_dev(lo), nat.to_dev(hi), nat.to_dev(op))
+            else:
+                shape, edges = grid
+                g = ("grid", len(shape), nat.to_dev(np.asarray(shape, dtype=np.int32)),
+                     nat.to_dev(np.concatenate(edges)))
             object.__setattr__(self, "_grid_cache", g)
         return g
 
@@ -207,13 +209,15 @@ class GlobalSurrogate:
         """K4 on device-resident points (P, dim) float64; returns a device tensor.
 
         Raises like the reference: ValueError for a point outside all boxes
-        (first index), FloatingPointError for a degenerate denominator.
+        (first index) or inside two boxes, FloatingPointError for a degenerate
+        denominator.
         """
         from . import _native as nat
 
         torch = nat.torch_mod()
         ds = self._device()
-        dim, d_shape, d_edges = self._grid_dev()
+        geo = self._grid_dev()
+        dim = geo[1]
         P = int(d_pts.shape[0])
         S = self.partition.n_subdomains
         if out is None:
@@ -222,12 +226,23 @@ class GlobalSurrogate:
             work = torch.empty(int(nat.lib().pam_eval_workspace_bytes(P, S)), dtype=torch.uint8,
                                device=d_pts.device)
         err = nat.ErrorWord()
-        nat.check(nat.lib().pam_eval_f64(
-            dim, P, nat.ptr(d_pts), nat.ptr(d_shape), nat.ptr(d_edges), S, nat.ptr(ds.d_dict_off),
-            nat.ptr(ds.d_m_cur), nat.ptr(ds.d_centres), nat.ptr(ds.d_widths), nat.ptr(ds.d_beta),
-            nat.ptr(ds.d_log), nat.ptr(out), nat.ptr(work), nat.ptr(err.t), nat.stream_ptr()),
-            "pam_eval_f64")
+        if geo[0] == "grid":
+            nat.check(nat.lib().pam_eval_f64(
+                dim, P, nat.ptr(d_pts), nat.ptr(geo[2]), nat.ptr(geo[3]), S, nat.ptr(ds.d_dict_off),
+                nat.ptr(ds.d_m_cur), nat.ptr(ds.d_centres), nat.ptr(ds.d_widths), nat.ptr(ds.d_beta),
+                nat.ptr(ds.d_log), nat.ptr(out), nat.ptr(work), nat.ptr(err.t), nat.stream_ptr()),
+                "pam_eval_f64")
+        else:
+            nat.check(nat.lib().pam_eval_boxes_f64(
+                dim, P, nat.ptr(d_pts), nat.ptr(geo[2]), nat.ptr(geo[3]), nat.ptr(geo[4]), S,
+                nat.ptr(ds.d_dict_off), nat.ptr(ds.d_m_cur), nat.ptr(ds.d_centres), nat.ptr(ds.d_widths),
+                nat.ptr(ds.d_beta), nat.ptr(ds.d_log), nat.ptr(out), nat.ptr(work), nat.ptr(err.t),
+                nat.stream_ptr()), "pam_eval_boxes_f64")
         code, j = err.read()
+        if code == nat.PAM_ERR_CLAIMED:
+            from .geometry import raise_claimed
+
+            raise_claimed(j, d_pts.cpu().numpy(), self.partition.boxes)  # error path: host copy is fine
         if code == nat.PAM_ERR_OUTSIDE:
             pt = d_pts[j].cpu().numpy().tolist()
             raise ValueError(f"point index {j} = {pt} lies outside all boxes")

@@ -316,6 +316,52 @@ def test_evaluate_order_positivity_and_errors(cuda):
     np.testing.assert_array_equal(surrogate.evaluate(pts), back.evaluate(pts))
 
 
+def _lshape_partition(mesh):
+    """Three boxes tiling [0,1]^2 that are NOT a tensor grid: the left half, and the
+    right half split in two (half-open internal faces, closed outer faces)."""
+    boxes = (pam.Box(lo=(0.0, 0.0), hi=(0.5, 1.0), open_hi=(True, False)),
+             pam.Box(lo=(0.5, 0.0), hi=(1.0, 0.5), open_hi=(False, True)),
+             pam.Box(lo=(0.5, 0.5), hi=(1.0, 1.0), open_hi=(False, False)))
+    cen = mesh.centroids
+    owner = O.locate_many(cen, [(b.lo, b.hi, b.open_hi) for b in boxes])
+    return pam.Partition(mesh=mesh, shape=(3,), boxes=boxes, cell_to_subdomain=owner)
+
+
+def test_generic_boxes_locate_evaluate_and_errors(cuda):
+    """Box sets that are not a tensor grid (the reference's locate_many and
+    GlobalSurrogate.evaluate accept any half-open boxes, geometry.py:242-258)."""
+    field = pam.box_field_2d(8, 8)
+    part = _lshape_partition(field.mesh)
+    assert part.grid is None
+    rng = np.random.default_rng(7)
+    pts = np.vstack([rng.random((500, 2)),
+                     [[0.5, 0.25], [0.5, 0.5], [0.75, 0.5], [1.0, 1.0], [0.0, 0.0], [0.5, 1.0], [1.0, 0.5]]])
+    boxes_o = [(b.lo, b.hi, b.open_hi) for b in part.boxes]
+    own_ref = O.locate_many(pts, boxes_o)
+    np.testing.assert_array_equal(pam.locate_many(pts, part.boxes), own_ref)  # faces included, bit-exact
+    surrogate, _ = pam.fit_parallel(field, part, PLAIN_CFG, pam.DictionarySpec(sigma=0.13))
+    vals = surrogate.evaluate(pts)
+    for i in range(part.n_subdomains):
+        sel = own_ref == i
+        np.testing.assert_array_equal(vals[sel], surrogate.locals[i].evaluate(pts[sel]))
+    ref, _ = O.global_evaluate(pts, boxes_o, [(l.dictionary.centers, l.dictionary.widths, l.beta)
+                                              for l in surrogate.locals])
+    np.testing.assert_allclose(vals, ref, rtol=1e-8)
+    # a point in no box: first offending index, as the reference reports it
+    with pytest.raises(ValueError, match=r"point index 2 = \[1.5, 0.5\] lies outside all boxes"):
+        surrogate.evaluate(np.array([[0.2, 0.2], [0.7, 0.7], [1.5, 0.5], [2.0, 2.0]]))
+    with pytest.raises(ValueError, match="point index 1 "):
+        pam.locate_many(np.array([[0.2, 0.2], [-0.1, 0.5]]), part.boxes)
+    # overlapping boxes: the first box, in order, that re-claims a point wins the report
+    over = part.boxes + (pam.Box(lo=(0.4, 0.4), hi=(0.6, 0.6), open_hi=(True, True)),)
+    p2 = np.array([[0.9, 0.9], [0.55, 0.55], [0.45, 0.45], [1.7, 0.0]])
+    with pytest.raises(ValueError) as e_gpu:
+        pam.locate_many(p2, over)
+    with pytest.raises(ValueError) as e_ref:
+        O.locate_many(p2, [(b.lo, b.hi, b.open_hi) for b in over])
+    assert str(e_gpu.value) == str(e_ref.value) == "point index 1 claimed by boxes 2 and 3"
+
+
 def test_continuity_near_internal_face(cuda):
     field = pam.box_field_2d(8, 8)
     part = pam.make_partition(field.mesh, 2, 1)

@@ -22,7 +22,7 @@ def declared_symbols():
 
 def test_library_exists_and_loads():
     lib = _native.load_library()
-    assert lib.pam_abi_version() == _native.ABI_VERSION == 2
+    assert lib.pam_abi_version() == _native.ABI_VERSION == 3
     assert lib.pam_cd_max_rows() >= 2**31 - 1  # no row envelope (elastic_net.py has none)
     assert lib.pam_cd_workspace_bytes(10, 5000, 700, 500, 1) == 256
     assert lib.pam_cd_workspace_bytes(1, 20000, 100, 20000, 0) == 256 + 8 * 20000
