@@ -459,6 +459,60 @@ def test_config1_convergent_solver_matches_reference(cuda, golden):
         assert abs(obj - float(g[f"s{s}_objective"])) <= 1e-8 * max(abs(float(g[f"s{s}_objective"])), 1e-300)
 
 
+@pytest.mark.parametrize("cells", [(32, 32), (20, 20)])
+@pytest.mark.parametrize("lattice", [1, 3, 4, 5, 7])
+@pytest.mark.parametrize("max_iters,tol", [(4000, 1e-7), (1, 1e-6), (37, 1e-300)])
+def test_blocked_kernel_edge_shapes_match_lean(cuda, cells, lattice, max_iters, tol):
+    """The blocked CD (cd_block.cu) on its corner shapes against the lean per-column
+    kernel: one column, a single block (the block follows itself across sweeps), 16
+    columns exactly, two and four blocks, lists of <= 8 and > 8 columns per worker
+    warp, 1,024 and 400 rows, early convergence, a single sweep and a sweep cap."""
+    field = pam.box_field_2d(*cells)
+    part = pam.make_partition(field.mesh, 1, 1)
+    en = pam.ElasticNetConfig(lam1=4.59e-4, lam2=1e-4, tol=tol, max_iters=max_iters)
+    cfg = pam.AdaptiveConfig(m_max=0, elastic=en)
+    spec = pam.DictionarySpec(sigma=0.6 / lattice, lattice=lattice)
+    with E.options(cd_form="residual", cd_kernel="lean"):
+        lean, rl = pam.fit_parallel(field, part, cfg, spec)
+    with E.options(cd_form="residual", cd_kernel="block"):
+        blk, rb = pam.fit_parallel(field, part, cfg, spec)
+    a, b = lean.locals[0], blk.locals[0]
+    assert a.beta.shape == b.beta.shape == (lattice * lattice,)
+    assert np.max(np.abs(a.beta - b.beta)) <= 1e-10 * max(1, np.abs(a.beta).max())
+    x, y = rl.rounds[0][0], rb.rounds[0][0]
+    assert abs(x.objective - y.objective) <= 1e-10 * abs(x.objective)
+    sl, sb = int(rl.device["sweeps"]), int(rb.device["sweeps"])  # one fit, one round
+    assert 1 <= sb <= max_iters
+    if lattice > 1 or tol >= 1e-7:  # (one column reaches a rounding-level step after two sweeps)
+        assert abs(sl - sb) <= 1
+    if max_iters == 4000:
+        assert sb < max_iters  # the stop rule fired before the cap
+    elif lattice > 1:
+        assert sb == max_iters
+
+
+def test_blocked_kernel_many_small_fits_match_lean(cuda):
+    """169 fits of 64 rows through the blocked CD: more fits than CTAs (the work queue
+    hands a CTA several fits in turn), two-tile fits (most worker warps own no row of
+    any column: empty lists), two refinement rounds."""
+    field = pam.box_field_2d(104, 104)
+    part = pam.make_partition(field.mesh, 13, 13)
+    cfg = pam.AdaptiveConfig(k_top=8, m_max=24, m_q=3, max_rounds=2, elastic=EN_2D,
+                             offsets=((0.0, 0.0), (-0.25, 0.0), (0.25, 0.0)))
+    spec = pam.DictionarySpec(sigma=0.5 / 104)
+    with E.options(cd_form="residual", cd_kernel="lean"):
+        lean, rl = pam.fit_parallel(field, part, cfg, spec)
+    with E.options(cd_form="residual", cd_kernel="block"):
+        blk, rb = pam.fit_parallel(field, part, cfg, spec)
+    for a, b in zip(lean.locals, blk.locals):
+        np.testing.assert_array_equal(a.dictionary.centers, b.dictionary.centers)
+        assert np.max(np.abs(a.beta - b.beta)) <= 1e-10 * max(1, np.abs(a.beta).max())
+    for ra, rb_ in zip(rl.rounds, rb.rounds):
+        for x, y in zip(ra, rb_):
+            assert (x.centers, x.added) == (y.centers, y.added)
+            assert abs(x.objective - y.objective) <= 1e-10 * abs(x.objective)
+
+
 @pytest.mark.parametrize("cells,px", [((32, 32), 1), ((24, 24), 2), ((40, 30), 1)])
 def test_pipelined_few_fit_kernel_matches_lean(cuda, cells, px):
     """The software-pipelined CD for few fits (lag-1 Gram correction, cd.cu
