@@ -80,6 +80,28 @@ def test_grid_edges_detection():
     assert pam.geometry.grid_edges(bad) is None
 
 
+def test_box_arrays_and_claimed_error_message():
+    """Host side of the arbitrary-box path (geometry.py:54-66, 242-258): the box set as the
+    C-ABI's (lo, hi, open_hi) arrays, and the reference's message for a doubly claimed point
+    rebuilt from the device's packed (second box << 40 | point) key."""
+    from paper_2605_16564_b200 import geometry as G
+
+    boxes = (pam.Box(lo=(0.0, 0.0), hi=(0.5, 1.0), open_hi=(True, False)),
+             pam.Box(lo=(0.5, 0.0), hi=(1.0, 1.0), open_hi=(False, False)),
+             pam.Box(lo=(0.4, 0.4), hi=(0.6, 0.6), open_hi=(True, True)))
+    assert G.grid_edges(boxes) is None
+    lo, hi, op = G.box_arrays(boxes)
+    assert lo.dtype == hi.dtype == np.float64 and op.dtype == np.int32
+    assert lo.flags.c_contiguous and lo.shape == hi.shape == op.shape == (3, 2)
+    np.testing.assert_array_equal(op, [[1, 0], [0, 0], [1, 1]])
+    np.testing.assert_array_equal(hi[2], [0.6, 0.6])
+    pts = np.array([[0.9, 0.9], [0.55, 0.55], [0.45, 0.45]])
+    with pytest.raises(ValueError, match="^point index 1 claimed by boxes 1 and 2$"):
+        G.raise_claimed((2 << 40) | 1, pts, boxes)
+    with pytest.raises(ValueError, match="^point index 2 claimed by boxes 0 and 2$"):
+        G.raise_claimed((2 << 40) | 2, pts, boxes)
+
+
 def test_dictionary_capacity_matches_reference_loop_bounds():
     # C4: 500 + min(2*300, 599+300) = 1100; m_max=0 -> no growth
     cap = engine.dictionary_capacity([500, 500], [100, 100], [3, 3], [600, 0], [3, 3])
