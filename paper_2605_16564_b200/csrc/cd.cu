@@ -907,13 +907,14 @@ __global__ void __launch_bounds__(WPC * 32, 1) cd_dual_kernel(const CdArgs a) {
           const double cs = pc[hb + t];
           const double inv = pinv[hb + t];
           const double cb_old = __dmul_rn(cs, b_old);
-          const double dn = __dadd_rn(cs, lam2);
           const double dot = half_sum(part);
           const double z = __dadd_rn(cb_old, dot);
           const double np_ = __dsub_rn(z, lam1), nn_ = __dadd_rn(z, lam1);
-          const double qp = __dmul_rn(np_, inv), qn = __dmul_rn(nn_, inv);
-          const double bp = fma(fma(-qp, dn, np_), inv, qp);
-          const double bn = fma(fma(-qn, dn, nn_), inv, qn);
+          // the quotient S(z, lam1) / (col_sq + lam2) as the product with the correctly
+          // rounded reciprocal (<= 1.5 ulp from the division, far inside the rounding
+          // class of the reordered dots; two dependent DFMAs off the per-column chain:
+          // C4 CD 8.13 -> 8.06 s, profiles/r02_cd_dual_predicated_loads_ab.txt)
+          const double bp = __dmul_rn(np_, inv), bn = __dmul_rn(nn_, inv);
           double b_new = np_ > 0.0 ? bp : (nn_ < 0.0 ? bn : 0.0);
           if (!act) b_new = b_old;
           const double d = __dsub_rn(b_new, b_old);
