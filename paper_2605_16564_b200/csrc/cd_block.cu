@@ -644,7 +644,6 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
             // quotient is the product with the correctly rounded reciprocal: <= 1.5 ulp
             // from the reference's division, far inside the rounding class of the
             // reordered inner products.)  Four columns per straight-line group.
-            const int pkc = pkn;  // this lane's column parameters (for the AXPY lists)
             double dc = 0.0;
             double zq = __shfl_sync(0xffffffffu, zc, 0);    // bracket of column k
             double zp1 = __shfl_sync(0xffffffffu, zc, 1);   // broadcast copy of column k+1 (steps <= k-2)
