@@ -562,7 +562,6 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
       double corr = 0.0;  // solver: G[t, t-1] d_{t-1} of this lane's column (accumulated during step t-1)
       double invc = 0.0;                // 1 / (col_sq + lam2) of this block's column
       double g1n = 0.0, g2n = 0.0;      // next block's G[c][c-1], G[c][c-2] (read from its slot a step early)
-      int pkn = 0;                      // next block's packed column parameters
       bool first_blk = true;
       int st_j = -1;      // deferred coefficient store: index (or -1) and value
       double st_b = 0.0;
@@ -617,14 +616,11 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
             {
               const bool on = lane < nb;
               double g1 = g1n, g2 = g2n;
-              int pk0 = pkn;
               if (first_blk) {
                 g1 = (on && lane > 0) ? Gd[(lane - 1) * nb + lane] : 0.0;
                 g2 = (on && lane > 1) ? Gd[(lane - 2) * nb + lane] : 0.0;
-                pk0 = par[32 * (t & 3) + lane];
                 first_blk = false;
               }
-              pkn = pk0;
               if (lane < 20) {
                 double2* sp = reinterpret_cast<double2*>(sprm + 4 * lane);
                 sp[0] = make_double2(on ? bc : 0.0, on ? invc : 0.0);
@@ -696,7 +692,6 @@ __global__ void __launch_bounds__(NT, MINB) cd_block_kernel(const CdArgs a, unsi
               const bool on1 = lane < nb1;
               g1n = (on1 && lane > 0) ? Gd1[(lane - 1) * nb1 + lane] : 0.0;
               g2n = (on1 && lane > 1) ? Gd1[(lane - 2) * nb1 + lane] : 0.0;
-              pkn = par[32 * ((t + 1) & 3) + lane];
             }
             PROF_LAP(3)
             // steps by column for the workers' AXPY (their per-warp column lists were built
